@@ -1,0 +1,184 @@
+/*
+ * posit_b200.h -- C ABI of libposit_b200.so: the Posit(32,2) hot path of the
+ * paper's posit-accelerated dense LU and Cholesky (arxiv 2401.14117,
+ * "Evaluation of POSIT Arithmetic with Accelerators") on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (LaTeX source), S:n = SPEC.md
+ * line n; "Q<k>" = the reading of an ambiguous passage listed in DESIGN.md.
+ *
+ * Data.  Matrices are ROW-MAJOR arrays of uint32_t Posit(32,2) bit patterns
+ * (Eq.1; 0x00000000 = 0, 0x80000000 = NaR, 0x40000000 = 1) with a
+ * leading dimension ld >= number of columns (reading Q13: the paper's
+ * MPLAPACK is column-major; BASELINE config 2 fixes row-major).  Element (i,j)
+ * of X is X[i*ldx + j].  Pivot vectors are int32_t, 1-based (LAPACK).
+ *
+ * Arithmetic.  Every multiply and every add is one correctly rounded
+ * Posit(32,2) operation: round to nearest, ties to even on the encoding (Q1),
+ * saturating at +-maxpos / +-minpos (Q2), NaR absorbing, x/0 = NaR,
+ * sqrt(x<0) = NaR (Q3).  There is no quire.  Order contract (Q6): every
+ * output element receives its products one at a time in ascending k,
+ *     c <- c (+/-) (a_ik (x) b_kj),
+ * so blocked, tiled and distributed executions are bit-identical to the
+ * textbook unblocked loops.
+ *
+ * Memory and streams.  Unless a function says HOST, every pointer is DEVICE
+ * memory allocated and owned by the caller; the library keeps no hidden
+ * persistent allocations.  `stream` is a cudaStream_t (NULL = legacy default
+ * stream).  All work is enqueued asynchronously on `stream`; no function
+ * synchronises the device except the *_host variants.  Results (including
+ * *info and ipiv) are valid once the stream has reached the enqueued work.
+ *
+ * Return codes.  0 = enqueued successfully.  -i = the i-th argument is invalid
+ * (LAPACK xerbla style).  POSIT_ENOTSUP = an unsupported option.  POSIT_ECUDA =
+ * a CUDA launch/API error (text via posit_last_error()).  Numerical failure
+ * (zero pivot, non-positive-definite minor) is never a return code: it is
+ * written to *info on the device.  NaR inputs are legal and propagate.
+ */
+#ifndef POSIT_B200_H
+#define POSIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POSIT_ABI_VERSION 1
+#define POSIT_OK 0
+#define POSIT_ENOTSUP (-100)
+#define POSIT_ECUDA (-101)
+
+#define POSIT_ONE 0x40000000u   /* +1 */
+#define POSIT_MONE 0xC0000000u  /* -1 */
+#define POSIT_NAR 0x80000000u
+
+/* Library version (POSIT_ABI_VERSION). */
+int posit_abi_version(void);
+
+/* Static description of a return code. */
+const char* posit_strerror(int code);
+
+/* Text of the last CUDA error seen by this thread ("" if none). */
+const char* posit_last_error(void);
+
+/*
+ * posit_gemm -- Eq.2: C <- alpha*op(A)*op(B) + beta*C in
+ * Posit(32,2), op(X) = X ('N') or X^T ('T').  op(A) is m x k, op(B) is k x n,
+ * C is m x n.  Per element: c <- (beta == 0 ? 0 : C_ij); for l = 0..k-1:
+ * c <- c (+) (+/-(op(A)_il (x) op(B)_lj)), sign = sign(alpha); C_ij <- c.
+ * With alpha = -1, beta = +1 this is the trailing-matrix update of the blocked
+ * LU, the hot path.
+ *   alpha  must be POSIT_ONE or POSIT_MONE (else -6); beta must be 0 or
+ *          POSIT_ONE (else -11) (reading Q7).
+ *   transa must be 'N' (transa = 'T' -> POSIT_ENOTSUP); transb 'N' or 'T'.
+ *   lda >= k, ldb >= n ('N') or >= k ('T'), ldc >= n.
+ * C must not overlap A or B.
+ */
+int posit_gemm(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+               const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
+               uint32_t* C, int64_t ldc, void* stream);
+
+/* Same contract and result as posit_gemm, computed by a one-thread-per-output
+ * kernel with the generic per-operation path (a parity cross-check; slow). */
+int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+                     const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
+                     uint32_t* C, int64_t ldc, void* stream);
+
+/* HOST variant of posit_gemm (end-to-end path): A, B, C are HOST arrays
+ * (pinned memory recommended); `dwork` is a DEVICE workspace of at least
+ * posit_gemm_host_work_bytes(m, n, k) bytes.  Copies A, B, C to the device,
+ * runs posit_gemm, copies C back and synchronises `stream`. */
+size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k);
+int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+                    const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
+                    uint32_t* C, int64_t ldc, void* dwork, size_t work_bytes, void* stream);
+
+/*
+ * posit_syrk -- lower triangle of C (n x n) <- alpha*A*A^T + beta*C, A n x k
+ * (uplo = 'L', trans = 'N' only), same per-element order as posit_gemm.  The
+ * Cholesky trailing update.  The strict upper triangle of C is
+ * neither read nor written.  alpha/beta as posit_gemm (-5 / -8).
+ */
+int posit_syrk(char uplo, char trans, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A, int64_t lda,
+               uint32_t beta, uint32_t* C, int64_t ldc, void* stream);
+
+/*
+ * posit_trsm -- triangular solve with multiple right-hand sides
+ * (S:206-214), alpha must be POSIT_ONE (else -7).  Supported:
+ *   side='L', uplo='L', transa='N', diag='U':  B (m x n) <- L^{-1} B, L m x m
+ *       unit lower: b_ij <- b_ij (-) l_ik (x) b_kj, k = 0..i-1 ascending.
+ *       (LU: U12 = L11^{-1} A12.)
+ *   side='R', uplo='L', transa='T', diag='N':  B (m x n) <- B L^{-T}, L n x n
+ *       lower: b_ij <- b_ij (-) b_ik (x) l_jk, k = 0..j-1 ascending, then
+ *       b_ij <- b_ij (/) l_jj.  (Cholesky: L21 = A21 L11^{-T}.)
+ * Other combinations return POSIT_ENOTSUP.  Only the referenced triangle of
+ * A is read.
+ */
+int posit_trsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, uint32_t alpha,
+               const uint32_t* A, int64_t lda, uint32_t* B, int64_t ldb, void* stream);
+
+/*
+ * posit_getrf -- blocked right-looking LU with partial pivoting of the m x n
+ * matrix A, block size nb.  Result bit-identical
+ * to the textbook kij loop: for k: p = argmax_{i>=k} abs(a_ik) by signed
+ * compare of patterns, ties -> smallest i (Q10); ipiv[k] = p+1; if a_pk != 0
+ * swap rows k and p across the full width and set a_ik <- a_ik (/) a_kk
+ * (one posit division, Q8) for i > k, else *info = first such k+1 (Q11, the
+ * factorisation continues); a_ij <- a_ij (-) a_ik (x) a_kj for i,j > k.
+ * On exit A holds L (unit, strictly lower) and U; ipiv (length min(m,n)) and
+ * info are DEVICE int32.  work may be NULL when posit_getrf_work_bytes() == 0.
+ */
+size_t posit_getrf_work_bytes(int64_t m, int64_t n, int64_t nb);
+int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t nb,
+                void* work, size_t work_bytes, void* stream);
+
+/*
+ * posit_getrf_panel -- unblocked LU with partial pivoting of the m x b panel
+ * A (the panel step of posit_getrf; used by the multi-GPU driver).  Row swaps
+ * are applied inside the panel only.  ipiv[j] receives row_base + p + 1
+ * (1-based, offset by row_base); *info, if still 0, receives row_base + j + 1
+ * at the first zero pivot.
+ */
+int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
+                      int64_t row_base, void* stream);
+
+/*
+ * posit_laswp -- apply the row interchanges ipiv[k1..k2) in order to columns
+ * [0, ncols) of A: for k = k1..k2-1, swap rows k and ipiv[k]-1-ipiv_base.
+ */
+int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
+                int64_t ipiv_base, void* stream);
+
+/*
+ * posit_potrf -- blocked right-looking Cholesky A = L L^T of the n x n SPD
+ * matrix (uplo = 'L' only), block size nb.
+ * Bit-identical to the textbook loop: for k: if signed(a_kk) <= 0 then
+ * *info = k+1 and stop (Q9); a_kk <- sqrt(a_kk); a_ik <- a_ik (/) a_kk;
+ * a_ij <- a_ij (-) a_ik (x) a_jk for k < j <= i.  The strict upper triangle is
+ * not referenced.  After a failure only *info and the columns of the blocks
+ * before the failing block are defined.
+ */
+size_t posit_potrf_work_bytes(int64_t n, int64_t nb);
+int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, int64_t nb, void* work,
+                size_t work_bytes, void* stream);
+
+/* Conversions: binary64 -> posit rounds once (RNE), NaN/Inf -> NaR,
+ * -0 -> 0, subnormals -> +-minpos; posit -> binary64 is exact (NaR -> NaN). */
+int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream);
+int posit_to_f64(const uint32_t* p, double* out, int64_t count, void* stream);
+
+/* Elementwise ops (Table tabrandom's Add/Mul/Div/Sqrt kernels):
+ * out[i] = a[i] op b[i]; op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt (b unused). */
+#define POSIT_OP_ADD 0
+#define POSIT_OP_SUB 1
+#define POSIT_OP_MUL 2
+#define POSIT_OP_DIV 3
+#define POSIT_OP_SQRT 4
+int posit_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POSIT_B200_H */

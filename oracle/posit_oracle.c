@@ -65,8 +65,6 @@ typedef struct {
 
 static uint32_t mask_n(int n) { return n == 32 ? 0xFFFFFFFFu : ((1u << n) - 1u); }
 
-static int floor_div(int a, int b) { int q = a / b; if ((a % b) != 0 && ((a < 0) != (b < 0))) q--; return q; }
-
 static int bitlen_u128(u128 x) {
     uint64_t hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
     if (hi) return 128 - __builtin_clzll(hi);
@@ -137,7 +135,7 @@ static uint32_t p_encode(int sign, u128 N, int X, int n, int es) {
         p = 1;                                   /* 0 < |x| <= minpos -> minpos */
     } else {
         const int useed_log = 1 << es;
-        const int k = floor_div(scale, useed_log);
+        const int k = scale >> es;               /* floor(scale / 2^es) */
         const int e = scale - k * useed_log;
         bitstr b = {0, 128, 0};
         if (k >= 0) bs_append(&b, ((((u128)1) << (k + 1)) - 1) << 1, k + 2);  /* 1..1 0 */

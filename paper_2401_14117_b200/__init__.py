@@ -1,0 +1,189 @@
+"""paper_2401_14117_b200 -- Posit(32,2) LU / Cholesky hot path on NVIDIA B200.
+
+Thin Python binding of the C ABI in ``include/posit_b200.h``
+(``libposit_b200.so``, built in-tree by ``paper_2401_14117_b200.build``).
+Every function here only marshals arguments -- torch tensors (uint32 patterns
+stored as int32, device memory) become raw pointers, the current torch CUDA
+stream becomes the ``cudaStream_t`` -- and calls the library of the same
+name.  All arithmetic runs in the CUDA kernels.  There is no CPU fallback:
+if the library or a CUDA device is missing, the calls raise.
+
+Posit patterns live in ``torch.int32`` tensors (torch has no uint32 arithmetic
+on CUDA); the bits are the Posit(32,2) encoding (0x40000000 = 1.0).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "lib", "PositError", "posit_gemm", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
+    "posit_getrf", "posit_getrf_panel", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
+    "posit_vec_op", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
+]
+
+POSIT_ONE = 0x40000000
+POSIT_MONE = 0xC0000000
+POSIT_NAR = 0x80000000
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libposit_b200.so")
+_lib = None
+
+
+class PositError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    """Load libposit_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PositError(f"{LIB_PATH} missing: run `python -m paper_2401_14117_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        c_char, i64, u32, vp, sz = ctypes.c_char, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
+        gemm_args = [c_char, c_char, i64, i64, i64, u32, vp, i64, vp, i64, u32, vp, i64, vp]
+        L.posit_gemm.argtypes = gemm_args
+        L.posit_gemm_naive.argtypes = gemm_args
+        L.posit_gemm_host.argtypes = gemm_args[:-1] + [vp, sz, vp]
+        L.posit_gemm_host_work_bytes.argtypes = [i64, i64, i64]
+        L.posit_gemm_host_work_bytes.restype = sz
+        L.posit_syrk.argtypes = [c_char, c_char, i64, i64, u32, vp, i64, u32, vp, i64, vp]
+        L.posit_trsm.argtypes = [c_char, c_char, c_char, c_char, i64, i64, u32, vp, i64, vp, i64, vp]
+        L.posit_getrf.argtypes = [i64, i64, vp, i64, vp, vp, i64, vp, sz, vp]
+        L.posit_getrf_work_bytes.argtypes = [i64, i64, i64]
+        L.posit_getrf_work_bytes.restype = sz
+        L.posit_getrf_panel.argtypes = [i64, i64, vp, i64, vp, vp, i64, vp]
+        L.posit_laswp.argtypes = [i64, vp, i64, i64, i64, vp, i64, vp]
+        L.posit_potrf.argtypes = [c_char, i64, vp, i64, vp, i64, vp, sz, vp]
+        L.posit_potrf_work_bytes.argtypes = [i64, i64]
+        L.posit_potrf_work_bytes.restype = sz
+        L.posit_from_f64.argtypes = [vp, vp, i64, vp]
+        L.posit_to_f64.argtypes = [vp, vp, i64, vp]
+        L.posit_vec_op.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp]
+        L.posit_strerror.argtypes = [ctypes.c_int]
+        L.posit_strerror.restype = ctypes.c_char_p
+        L.posit_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, name: str) -> None:
+    if rc != 0:
+        L = lib()
+        raise PositError(f"{name} returned {rc}: {L.posit_strerror(rc).decode()} {L.posit_last_error().decode()}")
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    if not t.is_cuda:
+        raise PositError("expected a CUDA tensor (device memory)")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ld(t) -> int:
+    return t.stride(0) if t.dim() == 2 else max(t.shape[-1], 1)
+
+
+def posit_gemm(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None,
+               transa: str = "N") -> None:
+    """C <- alpha*A*op(B) + beta*C in place (row-major int32 pattern tensors; views with row stride allowed)."""
+    m, k = A.shape
+    n = C.shape[1]
+    _check(lib().posit_gemm(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
+                            _ptr(C), _ld(C), _stream(stream)), "posit_gemm")
+
+
+def posit_gemm_naive(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None) -> None:
+    m, k = A.shape
+    n = C.shape[1]
+    _check(lib().posit_gemm_naive(b"N", transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
+                                  _ptr(C), _ld(C), _stream(stream)), "posit_gemm_naive")
+
+
+def posit_gemm_host(A, B, C, dwork, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE,
+                    stream=None) -> None:
+    """HOST-buffer GEMM: A, B, C are CPU (pinned) int32 tensors; dwork a CUDA byte workspace."""
+    m, k = A.shape
+    n = C.shape[1]
+    for t in (A, B, C):
+        if t.is_cuda or not t.is_contiguous():
+            raise PositError("posit_gemm_host expects contiguous host tensors")
+    _check(lib().posit_gemm_host(b"N", transb.encode(), m, n, k, alpha, A.data_ptr(), _ld(A), B.data_ptr(), _ld(B),
+                                 beta, C.data_ptr(), _ld(C), _ptr(dwork), dwork.numel() * dwork.element_size(),
+                                 _stream(stream)), "posit_gemm_host")
+
+
+def posit_gemm_host_work_bytes(m: int, n: int, k: int) -> int:
+    return int(lib().posit_gemm_host_work_bytes(m, n, k))
+
+
+def posit_syrk(A, C, alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None) -> None:
+    """Lower triangle of C <- alpha*A*A^T + beta*C."""
+    n, k = A.shape
+    _check(lib().posit_syrk(b"L", b"N", n, k, alpha, _ptr(A), _ld(A), beta, _ptr(C), _ld(C), _stream(stream)),
+           "posit_syrk")
+
+
+def posit_trsm(side: str, uplo: str, transa: str, diag: str, A, B, stream=None) -> None:
+    m, n = B.shape
+    _check(lib().posit_trsm(side.encode(), uplo.encode(), transa.encode(), diag.encode(), m, n, POSIT_ONE, _ptr(A),
+                            _ld(A), _ptr(B), _ld(B), _stream(stream)), "posit_trsm")
+
+
+def posit_getrf(A, ipiv, info, nb: int = 256, stream=None) -> None:
+    """In-place blocked LU with partial pivoting; ipiv (int32, min(m,n)) and info (int32, 1) are device tensors."""
+    m, n = A.shape
+    _check(lib().posit_getrf(m, n, _ptr(A), _ld(A), _ptr(ipiv), _ptr(info), nb, None, 0, _stream(stream)),
+           "posit_getrf")
+
+
+def posit_getrf_panel(P, ipiv, info, row_base: int = 0, stream=None) -> None:
+    m, b = P.shape
+    _check(lib().posit_getrf_panel(m, b, _ptr(P), _ld(P), _ptr(ipiv), _ptr(info), row_base, _stream(stream)),
+           "posit_getrf_panel")
+
+
+def posit_laswp(A, k1: int, k2: int, ipiv, ipiv_base: int = 0, stream=None) -> None:
+    ncols = A.shape[1]
+    _check(lib().posit_laswp(ncols, _ptr(A), _ld(A), k1, k2, _ptr(ipiv), ipiv_base, _stream(stream)), "posit_laswp")
+
+
+def posit_potrf(A, info, nb: int = 256, stream=None) -> None:
+    n = A.shape[0]
+    _check(lib().posit_potrf(b"L", n, _ptr(A), _ld(A), _ptr(info), nb, None, 0, _stream(stream)), "posit_potrf")
+
+
+def posit_from_f64(x, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    _check(lib().posit_from_f64(_ptr(x), _ptr(out), x.numel(), _stream(stream)), "posit_from_f64")
+    return out
+
+
+def posit_to_f64(p, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty(p.shape, dtype=torch.float64, device=p.device)
+    _check(lib().posit_to_f64(_ptr(p), _ptr(out), p.numel(), _stream(stream)), "posit_to_f64")
+    return out
+
+
+def posit_vec_op(op: str, a, b=None, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty_like(a)
+    _check(lib().posit_vec_op(OPS[op], _ptr(a), _ptr(a if b is None else b), _ptr(out), a.numel(), _stream(stream)),
+           "posit_vec_op")
+    return out

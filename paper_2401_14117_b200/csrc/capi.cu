@@ -1,0 +1,259 @@
+// capi.cu -- the C ABI of libposit_b200.so (include/posit_b200.h): argument
+// validation, the blocked getrf / potrf drivers, and the HOST-buffer GEMM.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include "gemm.cuh"
+#include "internal.h"
+
+static thread_local char g_last_error[256] = "";
+
+static int cuda_check(cudaError_t e) {
+  if (e == cudaSuccess) return 0;
+  strncpy(g_last_error, cudaGetErrorString(e), sizeof(g_last_error) - 1);
+  return POSIT_ECUDA;
+}
+
+static int launch_check(int rc) {
+  if (rc == POSIT_ECUDA) {
+    const cudaError_t e = cudaGetLastError();
+    strncpy(g_last_error, cudaGetErrorString(e), sizeof(g_last_error) - 1);
+  }
+  return rc;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int posit_abi_version(void) { return POSIT_ABI_VERSION; }
+
+const char* posit_strerror(int code) {
+  if (code == POSIT_OK) return "ok";
+  if (code == POSIT_ENOTSUP) return "unsupported option";
+  if (code == POSIT_ECUDA) return "CUDA error (see posit_last_error)";
+  if (code < 0 && code > -100) return "invalid argument";
+  return "unknown";
+}
+
+const char* posit_last_error(void) { return g_last_error; }
+
+static int gemm_common(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+                       int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
+                       void* stream, bool naive) {
+  if (transa != 'N' && transa != 'T') return -1;
+  if (transb != 'N' && transb != 'T') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  if (alpha != POSIT_ONE && alpha != POSIT_MONE) return -6;
+  if (transa == 'T') return POSIT_ENOTSUP;
+  if (lda < (k > 1 ? k : 1)) return -8;
+  if (ldb < ((transb == 'N' ? n : k) > 1 ? (transb == 'N' ? n : k) : 1)) return -10;
+  if (beta != 0u && beta != POSIT_ONE) return -11;
+  if (ldc < (n > 1 ? n : 1)) return -13;
+  if (m == 0 || n == 0) return 0;
+  if ((k > 0 && (A == nullptr || B == nullptr)) || C == nullptr) return -7;
+  pg::Params P{m, n, k, A, lda, B, ldb, C, ldc, alpha == POSIT_MONE ? 1 : 0, beta == POSIT_ONE ? 1 : 0, nullptr};
+  const int rc = naive ? pb_launch_gemm_naive(P, transb == 'T', false, S(stream))
+                       : pb_launch_gemm(P, transb == 'T', false, S(stream));
+  if (rc) return launch_check(rc);
+  return cuda_check(cudaPeekAtLastError());
+}
+
+int posit_gemm(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+               int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc, void* stream) {
+  return gemm_common(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, false);
+}
+
+int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+                     int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
+                     void* stream) {
+  return gemm_common(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, true);
+}
+
+size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k) {
+  if (m < 0 || n < 0 || k < 0) return 0;
+  return (size_t)4 * (size_t)(m * k + k * n + m * n) + 256;
+}
+
+int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+                    int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
+                    void* dwork, size_t work_bytes, void* stream) {
+  if (transa != 'N') return transa == 'T' ? POSIT_ENOTSUP : -1;
+  if (transb != 'N' && transb != 'T') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  if (work_bytes < posit_gemm_host_work_bytes(m, n, k) || dwork == nullptr) return -15;
+  const int64_t brow = transb == 'N' ? k : n, bcol = transb == 'N' ? n : k;
+  uint32_t* dA = reinterpret_cast<uint32_t*>(dwork);
+  uint32_t* dB = dA + m * k;
+  uint32_t* dC = dB + k * n;
+  cudaStream_t st = S(stream);
+  int rc;
+  if ((rc = cuda_check(cudaMemcpy2DAsync(dA, (size_t)k * 4, A, (size_t)lda * 4, (size_t)k * 4, (size_t)m,
+                                         cudaMemcpyHostToDevice, st))))
+    return rc;
+  if ((rc = cuda_check(cudaMemcpy2DAsync(dB, (size_t)bcol * 4, B, (size_t)ldb * 4, (size_t)bcol * 4, (size_t)brow,
+                                         cudaMemcpyHostToDevice, st))))
+    return rc;
+  if (beta != 0u) {
+    if ((rc = cuda_check(cudaMemcpy2DAsync(dC, (size_t)n * 4, C, (size_t)ldc * 4, (size_t)n * 4, (size_t)m,
+                                           cudaMemcpyHostToDevice, st))))
+      return rc;
+  }
+  rc = posit_gemm(transa, transb, m, n, k, alpha, dA, k > 0 ? k : 1, dB, bcol > 0 ? bcol : 1, beta, dC,
+                  n > 0 ? n : 1, stream);
+  if (rc) return rc;
+  if ((rc = cuda_check(cudaMemcpy2DAsync(C, (size_t)ldc * 4, dC, (size_t)n * 4, (size_t)n * 4, (size_t)m,
+                                         cudaMemcpyDeviceToHost, st))))
+    return rc;
+  return cuda_check(cudaStreamSynchronize(st));
+}
+
+int posit_syrk(char uplo, char trans, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A, int64_t lda,
+               uint32_t beta, uint32_t* C, int64_t ldc, void* stream) {
+  if (uplo != 'L' && uplo != 'U') return -1;
+  if (trans != 'N' && trans != 'T') return -2;
+  if (n < 0) return -3;
+  if (k < 0) return -4;
+  if (alpha != POSIT_ONE && alpha != POSIT_MONE) return -5;
+  if (lda < (k > 1 ? k : 1)) return -7;
+  if (beta != 0u && beta != POSIT_ONE) return -8;
+  if (ldc < (n > 1 ? n : 1)) return -10;
+  if (uplo != 'L' || trans != 'N') return POSIT_ENOTSUP;
+  if (n == 0) return 0;
+  pg::Params P{n, n, k, A, lda, A, lda, C, ldc, alpha == POSIT_MONE ? 1 : 0, beta == POSIT_ONE ? 1 : 0, nullptr};
+  const int rc = pb_launch_gemm(P, true, true, S(stream));
+  if (rc) return launch_check(rc);
+  return cuda_check(cudaPeekAtLastError());
+}
+
+int posit_trsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, uint32_t alpha, const uint32_t* A,
+               int64_t lda, uint32_t* B, int64_t ldb, void* stream) {
+  if (side != 'L' && side != 'R') return -1;
+  if (uplo != 'L' && uplo != 'U') return -2;
+  if (transa != 'N' && transa != 'T') return -3;
+  if (diag != 'N' && diag != 'U') return -4;
+  if (m < 0) return -5;
+  if (n < 0) return -6;
+  if (alpha != POSIT_ONE) return -7;
+  const int64_t ka = side == 'L' ? m : n;
+  if (lda < (ka > 1 ? ka : 1)) return -9;
+  if (ldb < (n > 1 ? n : 1)) return -11;
+  if (m == 0 || n == 0) return 0;
+  int rc;
+  if (side == 'L' && uplo == 'L' && transa == 'N' && diag == 'U') {
+    rc = pb_trsm_llnu(m, n, A, lda, B, ldb, S(stream));
+  } else if (side == 'R' && uplo == 'L' && transa == 'T' && diag == 'N') {
+    rc = pb_trsm_rltn(m, n, A, lda, B, ldb, nullptr, S(stream));
+  } else {
+    return POSIT_ENOTSUP;
+  }
+  return launch_check(rc);
+}
+
+size_t posit_getrf_work_bytes(int64_t m, int64_t n, int64_t nb) {
+  (void)m; (void)n; (void)nb;
+  return 0;
+}
+
+int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
+                      void* stream) {
+  if (m < 0) return -1;
+  if (b < 0) return -2;
+  if (lda < (b > 1 ? b : 1)) return -4;
+  if (m == 0 || b == 0) return 0;
+  return launch_check(pb_getrf_panel(m, b, A, lda, ipiv, info, row_base, nullptr, S(stream)));
+}
+
+int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
+                int64_t ipiv_base, void* stream) {
+  if (ncols < 0) return -1;
+  if (lda < (ncols > 1 ? ncols : 1)) return -3;
+  if (k1 < 0 || k2 < k1) return -4;
+  return launch_check(pb_laswp(ncols, A, lda, k1, k2, ipiv, ipiv_base, S(stream)));
+}
+
+int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t nb,
+                void* work, size_t work_bytes, void* stream) {
+  (void)work; (void)work_bytes;
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  if (nb < 1) return -7;
+  if (info == nullptr) return -6;
+  cudaStream_t st = S(stream);
+  int rc = cuda_check(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
+  if (rc) return rc;
+  const int64_t kmax = m < n ? m : n;
+  for (int64_t s = 0; s < kmax; s += nb) {
+    const int64_t b = (kmax - s) < nb ? (kmax - s) : nb;
+    // 1. panel: columns s..s+b, rows s..m
+    if ((rc = pb_getrf_panel(m - s, b, A + s * lda + s, lda, ipiv + s, info, s, nullptr, st))) return launch_check(rc);
+    // 2. the panel's swaps on the columns left and right of it
+    if (s > 0 && (rc = pb_laswp(s, A, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);
+    if (s + b < n && (rc = pb_laswp(n - s - b, A + s + b, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);
+    if (s + b < n) {
+      // 3. U12 = L11^{-1} A12
+      if ((rc = pb_trsm_llnu(b, n - s - b, A + s * lda + s, lda, A + s * lda + s + b, lda, st))) return launch_check(rc);
+      // 4. trailing update A22 -= L21 U12 (the hot path)
+      if (s + b < m) {
+        pg::Params P{m - s - b, n - s - b, b, A + (s + b) * lda + s, lda, A + s * lda + s + b, lda,
+                     A + (s + b) * lda + s + b, lda, 1, 1, nullptr};
+        if ((rc = pb_launch_gemm(P, false, false, st))) return launch_check(rc);
+      }
+    }
+  }
+  return cuda_check(cudaPeekAtLastError());
+}
+
+size_t posit_potrf_work_bytes(int64_t n, int64_t nb) {
+  (void)n; (void)nb;
+  return 0;
+}
+
+int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, int64_t nb, void* work,
+                size_t work_bytes, void* stream) {
+  (void)work; (void)work_bytes;
+  if (uplo != 'L' && uplo != 'U') return -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  if (info == nullptr) return -5;
+  if (nb < 1) return -6;
+  if (uplo != 'L') return POSIT_ENOTSUP;
+  cudaStream_t st = S(stream);
+  int rc = cuda_check(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
+  if (rc) return rc;
+  for (int64_t s = 0; s < n; s += nb) {
+    const int64_t b = (n - s) < nb ? (n - s) : nb;
+    if ((rc = pb_potf2(b, A + s * lda + s, lda, info, s, st))) return launch_check(rc);
+    if (s + b < n) {
+      if ((rc = pb_trsm_rltn(n - s - b, b, A + s * lda + s, lda, A + (s + b) * lda + s, lda, info, st)))
+        return launch_check(rc);
+      pg::Params P{n - s - b, n - s - b, b, A + (s + b) * lda + s, lda, A + (s + b) * lda + s, lda,
+                   A + (s + b) * lda + s + b, lda, 1, 1, info};
+      if ((rc = pb_launch_gemm(P, true, true, st))) return launch_check(rc);
+    }
+  }
+  return cuda_check(cudaPeekAtLastError());
+}
+
+int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream) {
+  if (count < 0) return -3;
+  return launch_check(pb_from_f64(x, out, count, S(stream)));
+}
+
+int posit_to_f64(const uint32_t* p, double* out, int64_t count, void* stream) {
+  if (count < 0) return -3;
+  return launch_check(pb_to_f64(p, out, count, S(stream)));
+}
+
+int posit_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream) {
+  if (op < POSIT_OP_ADD || op > POSIT_OP_SQRT) return -1;
+  if (count < 0) return -5;
+  return launch_check(pb_vec_op(op, a, b, out, count, S(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+// gemm.cu -- Posit(32,2) GEMM (NN, NT) and SYRK-lower kernels + launchers.
+// See gemm.cuh for the arithmetic and the order contract.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "gemm.cuh"
+#include "internal.h"
+
+namespace pg {
+
+// Tile configuration.  One CTA = BM x BN outputs, 256 threads, each thread a
+// TM x TN register tile of decoded accumulators; operands staged in k-slabs
+// of BK, double-buffered in shared memory as decoded (M, w) pairs.
+constexpr int BM = 64, BN = 128, BK = 16, TM = 8, TN = 4;
+constexpr int NTHR = (BM / TM) * (BN / TN);   // 256
+static_assert(NTHR == 256, "tile config");
+
+struct Smem {
+  uint2 a[2][BK][BM];
+  uint2 b[2][BK][BN];
+};
+
+// Generic per-operation MAC on patterns (the slow path; bit-identical to the
+// fast path by the contract).
+__device__ __forceinline__ uint32_t mac_generic(uint32_t c, uint32_t a, uint32_t b, int neg) {
+  const uint32_t p = p32::mul(a, b);
+  return p32::add(c, neg ? p32::neg(p) : p);
+}
+
+// Generic path over one k-slab for one accumulator (noinline and all-scalar
+// arguments: keeps the fast loop's accumulators in registers).  Returns the
+// new accumulator (x = M, y = E, z = s) and w = 1 if the result cannot live
+// in the fast accumulator.
+__device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, uint32_t sg, const uint32_t* A, int64_t lda,
+                                        const uint32_t* B, int64_t ldb, int neg, int64_t r, int64_t cc, int64_t k0,
+                                        int kmax, int transb) {
+  Acc acc{M, E, sg};
+  uint32_t c = acc_encode(acc);
+  for (int kk = 0; kk < kmax; kk++) {
+    const int64_t l = k0 + kk;
+    const uint32_t a = A[r * lda + l];
+    const uint32_t b = transb ? B[cc * ldb + l] : B[l * ldb + cc];
+    c = mac_generic(c, a, b, neg);
+  }
+  const uint32_t bad = acc_decode(c, acc) ? 0u : 1u;
+  return make_uint4(acc.M, (uint32_t)acc.E, acc.s, bad);
+}
+
+// Whole chain of one output with the generic path (the recompute of a thread
+// whose fast accumulator left the fast range).
+__device__ __noinline__ uint32_t slow_chain(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb,
+                                            const uint32_t* C, int64_t ldc, int beta, int neg, int64_t K, int64_t r,
+                                            int64_t cc, int transb) {
+  uint32_t c = beta ? C[r * ldc + cc] : 0u;
+  for (int64_t l = 0; l < K; l++) {
+    const uint32_t a = A[r * lda + l];
+    const uint32_t b = transb ? B[cc * ldb + l] : B[l * ldb + cc];
+    c = mac_generic(c, a, b, neg);
+  }
+  return c;
+}
+
+template <bool TRANS_B, bool SYRK>
+__global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN);          // 0..31 : column group (lane)
+  const int ty = tid / (BN / TN);          // 0..7  : row group (warp)
+  const int64_t row0 = (int64_t)blockIdx.y * BM;
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  if (SYRK && col0 > row0 + BM - 1) return;   // tile entirely above the diagonal
+  if (P.stop != nullptr && *P.stop != 0) return;
+
+  const uint32_t flip = P.neg ? 1u : 0u;
+
+  // ---- accumulators -------------------------------------------------------
+  Acc acc[TM][TN];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < TM; i++) {
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int64_t r = row0 + ty * TM + i, cc = col0 + tx * TN + j;
+      uint32_t cv = 0u;
+      if (P.beta && r < P.m && cc < P.n) cv = P.C[r * P.ldc + cc];
+      if (!acc_decode(cv, acc[i][j])) bad = true;
+    }
+  }
+
+  // ---- staging: A tile BM x BK (4 per thread), B tile BK x BN (8 per thread)
+  // A: thread -> (row ar, k offset ak4*4)
+  const int ar = tid / (BK / 4), ak = (tid % (BK / 4)) * 4;        // 64 rows x 4 quads
+  // B (NN): thread -> (k row bk, col quad) for two passes; B (NT): (col, k quad)
+  uint32_t ra[4], rb[8];
+
+  auto load_tile = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int64_t r = row0 + ar, kk = k0 + ak + q;
+      ra[q] = (r < P.m && kk < P.k) ? __ldg(P.A + r * P.lda + kk) : p32::ONE;
+    }
+    if (!TRANS_B) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int e = tid + h * NTHR;                 // 0..511 quads
+        const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int64_t kk = k0 + bk, cc = col0 + bc + q;
+          rb[h * 4 + q] = (kk < P.k && cc < P.n) ? __ldg(P.B + kk * P.ldb + cc) : p32::ONE;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int e = tid + h * NTHR;                 // 0..511 quads: (col, k quad)
+        const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int64_t kk = k0 + bk + q, cc = col0 + bc;
+          rb[h * 4 + q] = (kk < P.k && cc < P.n) ? __ldg(P.B + cc * P.ldb + kk) : p32::ONE;
+        }
+      }
+    }
+  };
+  auto store_tile = [&](int buf) -> uint32_t {
+    uint32_t sp = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[q], 0u, sp);
+    if (!TRANS_B) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int e = tid + h * NTHR;
+        const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30>(rb[h * 4 + q], flip, sp);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int e = tid + h * NTHR;
+        const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30>(rb[h * 4 + q], flip, sp);
+      }
+    }
+    return sp;
+  };
+
+  const int64_t ntiles = (P.k + BK - 1) / BK;
+  if (ntiles > 0) {
+    load_tile(0);
+  }
+  int special = ntiles > 0 ? __syncthreads_or((int)store_tile(0)) : 0;
+
+  for (int64_t t = 0; t < ntiles; t++) {
+    const int cur = (int)(t & 1);
+    const int64_t k0 = t * BK;
+    if (t + 1 < ntiles) load_tile(k0 + BK);
+    const int kmax = (int)min((int64_t)BK, P.k - k0);
+    if (!special) {
+      if (kmax == BK) {
+#pragma unroll 2
+        for (int kk = 0; kk < BK; kk++) {
+          uint2 av[TM], bv[TN];
+#pragma unroll
+          for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
+#pragma unroll
+          for (int j = 0; j < TN; j++) bv[j] = S.b[cur][kk][tx * TN + j];
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, bad);
+        }
+      } else {
+        for (int kk = 0; kk < kmax; kk++) {
+          uint2 av[TM], bv[TN];
+#pragma unroll
+          for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
+#pragma unroll
+          for (int j = 0; j < TN; j++) bv[j] = S.b[cur][kk][tx * TN + j];
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, bad);
+        }
+      }
+    } else if (!bad) {
+      // generic path for this k-slab (a zero / NaR / extreme operand is present)
+#pragma unroll
+      for (int i = 0; i < TM; i++) {
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+          const int64_t r = row0 + ty * TM + i, cc = col0 + tx * TN + j;
+          if (r < P.m && cc < P.n) {
+            const uint4 o = slow_slab(acc[i][j].M, acc[i][j].E, acc[i][j].s, P.A, P.lda, P.B, P.ldb, P.neg, r, cc,
+                                      k0, kmax, TRANS_B ? 1 : 0);
+            acc[i][j].M = o.x; acc[i][j].E = (int32_t)o.y; acc[i][j].s = o.z; bad = bad | (o.w != 0u);
+          }
+        }
+      }
+    }
+    if (t + 1 < ntiles) special = __syncthreads_or((int)store_tile(cur ^ 1));
+  }
+
+  // ---- epilogue ------------------------------------------------------------
+  if (bad) {
+    // recompute this thread's outputs from scratch with the generic path
+    for (int e = 0; e < TM * TN; e++) {
+      const int64_t r = row0 + ty * TM + e / TN, cc = col0 + tx * TN + e % TN;
+      if (r < P.m && cc < P.n && (!SYRK || cc <= r)) P.C[r * P.ldc + cc] = slow_chain(P.A, P.lda, P.B, P.ldb, P.C, P.ldc, P.beta, P.neg, P.k, r, cc, TRANS_B ? 1 : 0);
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < TM; i++) {
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int64_t r = row0 + ty * TM + i, cc = col0 + tx * TN + j;
+      if (r < P.m && cc < P.n && (!SYRK || cc <= r)) P.C[r * P.ldc + cc] = acc_encode(acc[i][j]);
+    }
+  }
+}
+
+// Naive reference kernel: one thread per output, generic per-operation path.
+__global__ void k_gemm_naive(Params P, int transb, int syrk) {
+  const int64_t cc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = blockIdx.y;
+  if (r >= P.m || cc >= P.n || (syrk && cc > r)) return;
+  if (P.stop != nullptr && *P.stop != 0) return;
+  uint32_t c = P.beta ? P.C[r * P.ldc + cc] : 0u;
+  for (int64_t l = 0; l < P.k; l++) {
+    const uint32_t a = P.A[r * P.lda + l];
+    const uint32_t b = transb ? P.B[cc * P.ldb + l] : P.B[l * P.ldb + cc];
+    c = mac_generic(c, a, b, P.neg);
+  }
+  P.C[r * P.ldc + cc] = c;
+}
+
+}  // namespace pg
+
+// ---- launchers (called from capi.cu) ----------------------------------------
+int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+  using namespace pg;
+  if (P.m == 0 || P.n == 0) return 0;
+  const dim3 grid((unsigned)((P.n + BN - 1) / BN), (unsigned)((P.m + BM - 1) / BM));
+  if (grid.y > 65535u) return PB_ERR_TOO_LARGE;
+  const size_t smem = sizeof(Smem);
+  static bool attr_done[4] = {false, false, false, false};
+  auto kern = transb ? (syrk ? k_gemm<true, true> : k_gemm<true, false>) : (syrk ? k_gemm<false, true> : k_gemm<false, false>);
+  const int idx = (transb ? 2 : 0) + (syrk ? 1 : 0);
+  if (!attr_done[idx]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_done[idx] = true;
+  }
+  kern<<<grid, NTHR, smem, st>>>(P);
+  return 0;
+}
+
+int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+  if (P.m == 0 || P.n == 0) return 0;
+  const dim3 grid((unsigned)((P.n + 127) / 128), (unsigned)P.m);
+  if (P.m > 65535) return PB_ERR_TOO_LARGE;
+  pg::k_gemm_naive<<<grid, 128, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
+  return 0;
+}

@@ -1,0 +1,26 @@
+// internal.h -- declarations shared by the .cu files of libposit_b200 (not public).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/posit_b200.h"
+
+#define PB_ERR_TOO_LARGE POSIT_ENOTSUP
+
+namespace pg { struct Params; }
+
+int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
+int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
+
+// lapack.cu
+int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
+                   int64_t row_base, const int32_t* stop_flag, cudaStream_t st);
+int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
+             int64_t ipiv_base, cudaStream_t st);
+int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st);
+int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                 const int32_t* stop_flag, cudaStream_t st);
+int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_base, cudaStream_t st);
+int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, cudaStream_t st);
+int pb_from_f64(const double* x, uint32_t* out, int64_t count, cudaStream_t st);
+int pb_to_f64(const uint32_t* p, double* out, int64_t count, cudaStream_t st);
+int pb_gemm_guarded(const pg::Params& P, bool transb, bool syrk, const int32_t* stop_flag, cudaStream_t st);

@@ -1,0 +1,117 @@
+"""GPU parity of posit_gemm / posit_syrk (the hot path) with the CPU oracle,
+element by element, through the C ABI.  Sizes span several 64x128 tiles and
+16-deep k-slabs with ragged tails; the full config-2 size is checked on
+sampled outputs the oracle computes one by one."""
+import numpy as np
+import pytest
+
+import synthetic_inputs as SI
+from oracle import oracle as O
+from tests.gpu_util import mismatch, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+ONE, MONE = O.P32_ONE, O.P32_MONE
+
+
+def _pats(x):
+    return O.from_f64_array(x)
+
+
+def _gpu_gemm(A, B, C, transb="N", alpha=MONE, beta=ONE, naive=False):
+    import paper_2401_14117_b200 as PB
+    dA, dB, dC = to_dev(A), to_dev(B), to_dev(C)
+    f = PB.posit_gemm_naive if naive else PB.posit_gemm
+    f(dA, dB, dC, transb=transb, alpha=alpha, beta=beta)
+    return to_host(dC)
+
+
+SHAPES = [(1, 1, 1), (3, 5, 7), (64, 128, 16), (67, 131, 45), (130, 257, 64), (200, 129, 300), (257, 300, 33)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("transb", ["N", "T"])
+def test_gemm_matches_oracle(cuda_ok, m, n, k, transb):
+    A, B, C = SI.config2(n=n, m=m, k=k)
+    if transb == "T":
+        B = B.T.copy()
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    ref = O.gemm(A, B, C, transb=transb)
+    assert mismatch(_gpu_gemm(A, B, C, transb), ref) == 0
+    assert mismatch(_gpu_gemm(A, B, C, transb, naive=True), ref) == 0
+
+
+@pytest.mark.parametrize("alpha,beta", [(ONE, ONE), (ONE, 0), (MONE, 0)])
+def test_gemm_alpha_beta(cuda_ok, alpha, beta):
+    A, B, C = SI.config2(n=96, m=70, k=50)
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    assert mismatch(_gpu_gemm(A, B, C, alpha=alpha, beta=beta), O.gemm(A, B, C, alpha=alpha, beta=beta)) == 0
+
+
+def test_gemm_special_values_and_cancellation(cuda_ok):
+    # zeros, NaR, huge/tiny magnitudes (slow k-slabs), exact cancellations (integers)
+    rng = np.random.default_rng(3)
+    m, n, k = 70, 140, 80
+    A = rng.integers(-3, 4, (m, k)).astype(np.float64)
+    B = rng.integers(-3, 4, (k, n)).astype(np.float64)
+    C = rng.integers(-5, 6, (m, n)).astype(np.float64)
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
+    A2 = _pats(SI.normal_matrix((m, k), 1.0, 4))
+    A2[5, 7] = O.P32_NAR
+    A2[9, :] = 0
+    A2[11, 3] = O.from_f64(1e30)
+    A2[12, 40] = O.from_f64(1e-33)
+    B2 = _pats(SI.normal_matrix((k, n), 1e3, 5))
+    C2 = _pats(SI.normal_matrix((m, n), 1e20, 6))        # accumulators beyond the fast range
+    C2[:, 0] = O.from_f64(2.0 ** 110)
+    assert mismatch(_gpu_gemm(A2, B2, C2), O.gemm(A2, B2, C2)) == 0
+
+
+@pytest.mark.parametrize("sigma", [1e-2, 1.0, 1e2, 1e4, 1e6])
+def test_gemm_sigma_sweep(cuda_ok, sigma):
+    # Fig gemm_v100's operand scales: same bits at every sigma
+    A = _pats(SI.normal_matrix((90, 60), sigma, 1))
+    B = _pats(SI.normal_matrix((60, 150), sigma, 2))
+    C = _pats(SI.normal_matrix((90, 150), sigma, 3))
+    assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
+
+
+def test_gemm_config2_full_size_sampled(cuda_ok):
+    # configs[1]: m=n=k=4096, N(0,1) seed 1, C -= A B; the oracle computes 24 x 24 sampled outputs
+    import torch
+    import paper_2401_14117_b200 as PB
+    A, B, C = SI.config2()
+    dA = PB.posit_from_f64(torch.from_numpy(A).cuda())
+    dB = PB.posit_from_f64(torch.from_numpy(B).cuda())
+    dC = PB.posit_from_f64(torch.from_numpy(C).cuda())
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(4096, 24, replace=False))
+    cols = np.sort(rng.choice(4096, 24, replace=False))
+    # the conversion itself must agree with the oracle's on the sampled operands
+    Ap, Bp, Cp = _pats(A[rows]), _pats(B[:, cols]), _pats(C[np.ix_(rows, cols)])
+    assert mismatch(to_host(dA)[rows], Ap) == 0
+    PB.posit_gemm(dA, dB, dC)
+    got = to_host(dC)[np.ix_(rows, cols)]
+    assert mismatch(got, O.gemm(Ap, Bp, Cp)) == 0
+
+
+def test_syrk_matches_oracle_and_keeps_upper(cuda_ok):
+    import paper_2401_14117_b200 as PB
+    for n, k in [(1, 3), (70, 33), (200, 256), (129, 17)]:
+        A = _pats(SI.normal_matrix((n, k), 1.0, n))
+        C = _pats(SI.config3(n))
+        ref = O.syrk_lower(A, C)
+        dC = to_dev(C)
+        PB.posit_syrk(to_dev(A), dC)
+        got = to_host(dC)
+        assert mismatch(got, ref) == 0
+
+
+def test_gemm_bad_arguments(cuda_ok):
+    import paper_2401_14117_b200 as PB
+    A = to_dev(_pats(np.ones((4, 4))))
+    with pytest.raises(PB.PositError):
+        PB.posit_gemm(A, A, A, alpha=O.from_f64(2.0))
+    with pytest.raises(PB.PositError):
+        PB.posit_gemm(A, A, A, beta=O.from_f64(0.5))

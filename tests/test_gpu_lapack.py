@@ -1,0 +1,116 @@
+"""GPU parity of posit_trsm / posit_getrf / posit_potrf with the CPU oracle
+(textbook unblocked loops), bit-exact on every output word, ipiv and info."""
+import numpy as np
+import pytest
+
+import synthetic_inputs as SI
+from oracle import oracle as O
+from tests.gpu_util import mismatch, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+def _pats(x):
+    return O.from_f64_array(x)
+
+
+def _gpu_getrf(A, nb):
+    import torch
+    import paper_2401_14117_b200 as PB
+    dA = to_dev(A)
+    m, n = A.shape
+    ipiv = torch.zeros(min(m, n), dtype=torch.int32, device="cuda")
+    info = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    PB.posit_getrf(dA, ipiv, info, nb=nb)
+    return to_host(dA), ipiv.cpu().numpy(), int(info.cpu()[0])
+
+
+def _gpu_potrf(A, nb):
+    import torch
+    import paper_2401_14117_b200 as PB
+    dA = to_dev(A)
+    info = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    PB.posit_potrf(dA, info, nb=nb)
+    return to_host(dA), int(info.cpu()[0])
+
+
+def test_trsm_llnu_matches_oracle(cuda_ok):
+    import paper_2401_14117_b200 as PB
+    for m, n in [(1, 5), (37, 100), (256, 300)]:
+        L = _pats(np.tril(SI.lu_matrix(m, 1), -1) + np.eye(m))
+        B = _pats(SI.normal_matrix((m, n), 1.0, 2))
+        dB = to_dev(B)
+        PB.posit_trsm("L", "L", "N", "U", to_dev(L), dB)
+        assert mismatch(to_host(dB), O.trsm_llnu(L, B)) == 0
+
+
+def test_trsm_rltn_matches_oracle(cuda_ok):
+    import paper_2401_14117_b200 as PB
+    for m, n in [(5, 1), (100, 37), (300, 256)]:
+        L = _pats(np.tril(SI.lu_matrix(n, 1), -1) + np.diag(1.0 + np.arange(n) % 3))
+        B = _pats(SI.normal_matrix((m, n), 1.0, 2))
+        dB = to_dev(B)
+        PB.posit_trsm("R", "L", "T", "N", to_dev(L), dB)
+        assert mismatch(to_host(dB), O.trsm_rltn(L, B)) == 0
+
+
+def test_getrf_config1_bit_exact(cuda_ok):
+    # configs[0]: n = 256, nb = 32, U[-1,1) seed 0
+    A = _pats(SI.config1())
+    ref, rpiv, rinfo = O.getrf(A)
+    got, piv, info = _gpu_getrf(A, 32)
+    assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv) and info == rinfo == 0
+
+
+@pytest.mark.parametrize("m,n,nb", [(100, 77, 16), (77, 100, 16), (300, 300, 64), (64, 64, 1), (130, 130, 256)])
+def test_getrf_ragged_and_block_sizes(cuda_ok, m, n, nb):
+    A = _pats(np.random.default_rng(m + n).uniform(-1, 1, (m, n)))
+    ref, rpiv, rinfo = O.getrf(A)
+    got, piv, info = _gpu_getrf(A, nb)
+    assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv) and info == rinfo
+
+
+def test_getrf_special_cases(cuda_ok):
+    # S:231, identity, zero column (info), dyadic exact
+    got, piv, info = _gpu_getrf(_pats([[0.0, 1.0], [2.0, 3.0]]), 32)
+    assert list(piv) == [2, 2] and info == 0 and np.array_equal(O.to_f64_array(got), [[2, 3], [0, 1]])
+    got, piv, info = _gpu_getrf(_pats(np.eye(40)), 16)
+    assert np.array_equal(O.to_f64_array(got), np.eye(40)) and list(piv) == list(range(1, 41))
+    A = SI.lu_matrix(50, 3)
+    A[:, 20] = 0.0
+    Ap = _pats(A)
+    ref, rpiv, rinfo = O.getrf(Ap)
+    got, piv, info = _gpu_getrf(Ap, 16)
+    assert rinfo == info == 21 and mismatch(got, ref) == 0 and np.array_equal(piv, rpiv)
+
+
+@pytest.mark.parametrize("s", [-16, -4, 0, 4, 16])
+def test_getrf_config5_scaling_small(cuda_ok, s):
+    # configs[4] recipe (U[-1,1) seed 4 scaled by 2^s) at n = 384, nb = 64
+    A = _pats(np.ldexp(SI.lu_matrix(384, SI.C5_SEED), s))
+    ref, rpiv, rinfo = O.getrf(A)
+    got, piv, info = _gpu_getrf(A, 64)
+    assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv) and info == rinfo
+
+
+@pytest.mark.parametrize("n,nb", [(1, 1), (50, 16), (200, 64), (300, 256), (130, 32)])
+def test_potrf_matches_oracle(cuda_ok, n, nb):
+    A = _pats(SI.config3(n))
+    ref, rinfo = O.potrf_lower(A)
+    got, info = _gpu_potrf(A, nb)
+    il = np.tril_indices(n)
+    iu = np.triu_indices(n, 1)
+    assert info == rinfo == 0
+    assert mismatch(got[il], ref[il]) == 0
+    assert mismatch(got[iu], A[iu]) == 0           # strict upper triangle untouched
+
+
+def test_potrf_not_positive_definite(cuda_ok):
+    A = SI.config3(80)
+    A[45, 45] = -1.0
+    Ap = _pats(A)
+    ref, rinfo = O.potrf_lower(Ap)
+    got, info = _gpu_potrf(Ap, 16)
+    assert info == rinfo == 46
+    # the blocks before the failing block are fully defined and bit-identical
+    assert mismatch(np.tril(got)[:, :32], np.tril(ref)[:, :32]) == 0

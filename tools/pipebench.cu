@@ -1,0 +1,68 @@
+// pipebench.cu -- measured integer-pipe throughput on this GPU (warp-instructions
+// per SM per clock) for the instruction classes of the posit MAC.  Each thread
+// runs 8 independent chains; the instruction is forced with inline PTX and
+// checked in SASS.  Output: one JSON object.
+#include <cstdio>
+#include <cuda_runtime.h>
+#define ITERS 4096
+#define CH 8
+template <int OP>
+__global__ void kern(unsigned* out, unsigned seed, long long* cyc) {
+  unsigned r[CH];
+  for (int i = 0; i < CH; i++) r[i] = seed * (threadIdx.x + 1) + i;
+  unsigned b = seed ^ 0x1234567u, c = seed + 77u;
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+      if (OP == 0) asm volatile("add.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(b));
+      if (OP == 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 2) asm volatile("shf.l.wrap.b32 %0, %0, %0, %1;" : "+r"(r[i]) : "r"(c));
+      if (OP == 3) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 4) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 5) asm volatile("bfind.u32 %0, %0;" : "+r"(r[i]));
+      if (OP == 6) asm volatile("{.reg .pred p; setp.lt.u32 p, %0, %1; selp.b32 %0, %1, %2, p;}" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 7) { if (i & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+                     else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[i]) : "r"(b), "r"(c)); }
+      if (OP == 8) asm volatile("add.cc.u32 %0, %0, %1; addc.u32 %0, %0, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 9) asm volatile("setp.gt.u32 %%p1, %0, %1;" :: "r"(r[i]), "r"(b));
+    }
+  }
+  long long t1 = clock64();
+  unsigned acc = 0;
+  for (int i = 0; i < CH; i++) acc ^= r[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int OP>
+double run(const char* name, int per_instr, unsigned* out, long long* cyc, int nsm, bool last) {
+  const int threads = 1024, blocks = nsm * 2;
+  kern<OP><<<blocks, threads>>>(out, 3u, cyc);
+  cudaDeviceSynchronize();
+  long long h[4096];
+  cudaMemcpy(h, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+  double mx = 0;
+  for (int i = 0; i < blocks; i++) mx = h[i] > mx ? h[i] : mx;
+  // warp-instructions per SM per clock: 2 CTAs/SM x 32 warps x ITERS x CH x per_instr / cycles
+  double rate = 2.0 * 32 * ITERS * CH * per_instr / mx;
+  printf("  \"%s\": %.3f%s\n", name, rate, last ? "" : ",");
+  return rate;
+}
+int main() {
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  unsigned* out; long long* cyc;
+  cudaMalloc(&out, sizeof(unsigned) * nsm * 2 * 1024); cudaMalloc(&cyc, sizeof(long long) * 4096);
+  printf("{\n  \"units\": \"warp-instructions per SM per clock (issue limit 4)\",\n  \"sm_count\": %d,\n", nsm);
+  run<0>("add.u32", 1, out, cyc, nsm, false);
+  run<1>("lop3", 1, out, cyc, nsm, false);
+  run<2>("shf", 1, out, cyc, nsm, false);
+  run<3>("mad.lo (IMAD)", 1, out, cyc, nsm, false);
+  run<4>("mad.hi (IMAD.HI)", 1, out, cyc, nsm, false);
+  run<5>("bfind (FLO)", 1, out, cyc, nsm, false);
+  run<6>("setp+selp (ISETP+SEL)", 2, out, cyc, nsm, false);
+  run<7>("mad.lo/lop3 mix", 1, out, cyc, nsm, false);
+  run<8>("add.cc+addc", 2, out, cyc, nsm, true);
+  printf("}\n");
+  return 0;
+}
