@@ -2,21 +2,28 @@
 // See gemm.cuh for the arithmetic and the order contract.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "gemm.cuh"
 #include "internal.h"
 
 namespace pg {
 
-// Tile configuration.  One CTA = BM x BN outputs, 256 threads, each thread a
+// Tile configuration.  One CTA = BM x BN outputs, NTHR threads, each thread a
 // TM x TN register tile of decoded accumulators; operands staged in k-slabs
 // of BK, double-buffered in shared memory as decoded (M, w) pairs.
-constexpr int BM = 64, BN = 128, BK = 16, TM = 8, TN = 4;
-constexpr int NTHR = (BM / TM) * (BN / TN);   // 256
-static_assert(NTHR == 256, "tile config");
-
-struct Smem {
-  uint2 a[2][BK][BM];
-  uint2 b[2][BK][BN];
+template <int BM_, int BN_, int TM_, int TN_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = 16, MINB = MINB_;
+  static constexpr int NTX = BN / TN, NTY = BM / TM, NTHR = NTX * NTY;
+  static constexpr int AQN = BM * BK / 4, BQN = BN * BK / 4;    // quads per tile
+  static constexpr int AQ = (AQN + NTHR - 1) / NTHR;            // A quads per thread (last may idle)
+  static constexpr int BQ = (BQN + NTHR - 1) / NTHR;
+  struct Smem {
+    uint2 a[2][BK][BM];
+    uint2 b[2][BK][BN];
+    uint2 tp[TSIZE];
+    uint2 tx[TSIZE];
+  };
 };
 
 // Generic per-operation MAC on patterns (the slow path; bit-identical to the
@@ -59,24 +66,30 @@ __device__ __noinline__ uint32_t slow_chain(const uint32_t* A, int64_t lda, cons
   return c;
 }
 
-template <bool TRANS_B, bool SYRK>
-__global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
+template <class C, bool TRANS_B, bool SYRK>
+__global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, TM = C::TM, TN = C::TN, NTHR = C::NTHR;
+  constexpr int AQ = C::AQ, BQ = C::BQ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(smem_raw);
 
   const int tid = threadIdx.x;
-  const int tx = tid % (BN / TN);          // 0..31 : column group (lane)
-  const int ty = tid / (BN / TN);          // 0..7  : row group (warp)
+  const int tx = tid % C::NTX;             // column group
+  const int ty = tid / C::NTX;             // row group
   const int64_t row0 = (int64_t)blockIdx.y * BM;
   const int64_t col0 = (int64_t)blockIdx.x * BN;
   if (SYRK && col0 > row0 + BM - 1) return;   // tile entirely above the diagonal
   if (P.stop != nullptr && *P.stop != 0) return;
 
   const uint32_t flip = P.neg ? 1u : 0u;
+  fill_tables(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
+  const uint2* tabp = S.tp + TBIAS;
+  const uint2* tabx = S.tx + TBIAS;
 
   // ---- accumulators -------------------------------------------------------
   Acc acc[TM][TN];
   bool bad = false;
+  uint32_t badacc = 0u;
 #pragma unroll
   for (int i = 0; i < TM; i++) {
 #pragma unroll
@@ -88,33 +101,33 @@ __global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
     }
   }
 
-  // ---- staging: A tile BM x BK (4 per thread), B tile BK x BN (8 per thread)
-  // A: thread -> (row ar, k offset ak4*4)
-  const int ar = tid / (BK / 4), ak = (tid % (BK / 4)) * 4;        // 64 rows x 4 quads
-  // B (NN): thread -> (k row bk, col quad) for two passes; B (NT): (col, k quad)
-  uint32_t ra[4], rb[8];
+  // ---- staging: A tile BM x BK and B tile BK x BN, in quads of 4 words
+  uint32_t ra[AQ * 4], rb[BQ * 4];
 
   auto load_tile = [&](int64_t k0) {
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int64_t r = row0 + ar, kk = k0 + ak + q;
-      ra[q] = (r < P.m && kk < P.k) ? __ldg(P.A + r * P.lda + kk) : p32::ONE;
-    }
-    if (!TRANS_B) {
+    for (int h = 0; h < AQ; h++) {
+      const int e = tid + h * NTHR;                   // (row, k quad)
+      if (e >= C::AQN) break;
+      const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int e = tid + h * NTHR;                 // 0..511 quads
+      for (int q = 0; q < 4; q++) {
+        const int64_t r = row0 + ar, kk = k0 + ak + q;
+        ra[h * 4 + q] = (r < P.m && kk < P.k) ? __ldg(P.A + r * P.lda + kk) : p32::ONE;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < BQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::BQN) break;
+      if (!TRANS_B) {                                 // (k row, col quad)
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
 #pragma unroll
         for (int q = 0; q < 4; q++) {
           const int64_t kk = k0 + bk, cc = col0 + bc + q;
           rb[h * 4 + q] = (kk < P.k && cc < P.n) ? __ldg(P.B + kk * P.ldb + cc) : p32::ONE;
         }
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int e = tid + h * NTHR;                 // 0..511 quads: (col, k quad)
+      } else {                                        // (col, k quad)
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -127,19 +140,22 @@ __global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
   auto store_tile = [&](int buf) -> uint32_t {
     uint32_t sp = 0u;
 #pragma unroll
-    for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[q], 0u, sp);
-    if (!TRANS_B) {
+    for (int h = 0; h < AQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::AQN) break;
+      const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int e = tid + h * NTHR;
+      for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+    }
+#pragma unroll
+    for (int h = 0; h < BQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::BQN) break;
+      if (!TRANS_B) {
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
 #pragma unroll
         for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30>(rb[h * 4 + q], flip, sp);
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int e = tid + h * NTHR;
+      } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
 #pragma unroll
         for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30>(rb[h * 4 + q], flip, sp);
@@ -171,7 +187,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, bad);
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, tabp, tabx, badacc);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
@@ -183,9 +199,16 @@ __global__ void __launch_bounds__(NTHR, 1) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, bad);
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, tabp, tabx, badacc);
         }
       }
+      // once per k-slab: fold the accumulated flags, bound the scales (table range)
+      bad = bad | (badacc >= BAD_FLAG);
+      badacc = 0u;
+#pragma unroll
+      for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) acc[i][j].E = min(acc[i][j].E, E_CLAMP);
     } else if (!bad) {
       // generic path for this k-slab (a zero / NaR / extreme operand is present)
 #pragma unroll
@@ -241,21 +264,51 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
 }  // namespace pg
 
 // ---- launchers (called from capi.cu) ----------------------------------------
-int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
-  using namespace pg;
-  if (P.m == 0 || P.n == 0) return 0;
-  const dim3 grid((unsigned)((P.n + BN - 1) / BN), (unsigned)((P.m + BM - 1) / BM));
+namespace {
+using V0 = pg::Cfg<64, 128, 8, 4, 1>;    // 256 thr, 32 accumulators / thread
+using V1 = pg::Cfg<64, 64, 4, 4, 2>;     // 256 thr, 16 acc, 2 CTAs / SM
+using V2 = pg::Cfg<64, 128, 4, 4, 1>;    // 512 thr, 16 acc
+using V3 = pg::Cfg<32, 128, 4, 4, 2>;    // 256 thr, 16 acc, 2 CTAs / SM
+using V4 = pg::Cfg<32, 128, 2, 4, 3>;    // 256 thr, 8 acc, 3 CTAs / SM
+using V5 = pg::Cfg<64, 128, 4, 8, 1>;    // 256 thr, 32 acc (TN = 8)
+
+template <class C>
+int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+  const dim3 grid((unsigned)((P.n + C::BN - 1) / C::BN), (unsigned)((P.m + C::BM - 1) / C::BM));
   if (grid.y > 65535u) return PB_ERR_TOO_LARGE;
-  const size_t smem = sizeof(Smem);
+  const size_t smem = sizeof(typename C::Smem);
   static bool attr_done[4] = {false, false, false, false};
-  auto kern = transb ? (syrk ? k_gemm<true, true> : k_gemm<true, false>) : (syrk ? k_gemm<false, true> : k_gemm<false, false>);
+  auto kern = transb ? (syrk ? pg::k_gemm<C, true, true> : pg::k_gemm<C, true, false>)
+                     : (syrk ? pg::k_gemm<C, false, true> : pg::k_gemm<C, false, false>);
   const int idx = (transb ? 2 : 0) + (syrk ? 1 : 0);
   if (!attr_done[idx]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done[idx] = true;
   }
-  kern<<<grid, NTHR, smem, st>>>(P);
+  kern<<<grid, C::NTHR, smem, st>>>(P);
   return 0;
+}
+
+int variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POSIT_GEMM_VARIANT");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+}  // namespace
+
+int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+  if (P.m == 0 || P.n == 0) return 0;
+  switch (variant()) {
+    case 1: return launch_cfg<V1>(P, transb, syrk, st);
+    case 2: return launch_cfg<V2>(P, transb, syrk, st);
+    case 3: return launch_cfg<V3>(P, transb, syrk, st);
+    case 4: return launch_cfg<V4>(P, transb, syrk, st);
+    case 5: return launch_cfg<V5>(P, transb, syrk, st);
+    default: return launch_cfg<V0>(P, transb, syrk, st);
+  }
 }
 
 int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {

@@ -19,8 +19,10 @@
 //  * rounding is RNE via two carry-chained adds (no masks, no branches);
 //  * a k-tile that contains a zero, NaR or |scale| > 53 operand is run by the
 //    generic per-operation path (uniform branch for the whole CTA); an
-//    accumulator whose sum leaves |E| <= 107 or cancels to exactly 0 marks the
-//    thread, which then recomputes its outputs with the generic path.  Both
+//    accumulator whose sum leaves |E| <= 107 marks the thread, which then
+//    recomputes its outputs with the generic path.  An exact cancellation
+//    (c (+) p == 0) stays in the fast path: the zero accumulator gets a scale
+//    far below any product.  Both
 //    are bit-identical by construction (same contract), and rare on the
 //    paper's workloads (N(0,1) / U[-1,1) data).
 #pragma once
@@ -66,30 +68,53 @@ struct Acc { uint32_t M; int32_t E; uint32_t s; };
 
 __device__ __forceinline__ uint32_t acc_encode(const Acc& c) {
   if (c.M == 0u) return 0u;
-  // M hidden at 30 -> S hidden at 63
-  return p32::round_encode(c.s, c.E, (uint64_t)c.M << 33);
+  // M hidden at 30 -> S hidden at 63; the sign is bit 0 of c.s
+  return p32::round_encode(c.s & 1u, c.E, (uint64_t)c.M << 33);
 }
 
 // returns false if the value cannot live in the fast accumulator (NaR, |E| > 107)
 __device__ __forceinline__ bool acc_decode(uint32_t x, Acc& c) {
-  if (x == 0u) { c.M = 0u; c.E = E_ZERO; c.s = 0u; return true; }
+  if (x == 0u) { c.M = 0u; c.E = E_ZERO; c.s = 0u; return true; }   // zero: far below any product
   const p32::Dec d = p32::decode(x);
   c.M = d.M >> 1; c.E = d.E; c.s = d.neg;
   return x != p32::NAR && d.E <= 107 && d.E >= -107;
 }
 
+// ---- rounding-position tables ---------------------------------------------
+// For a scale E the posit fraction width is f_s(E) = 27 - t(E) with
+// t(E) = (E ^ (E >> 31)) >> 2 (valid for |E| <= 107, f_s >= 1).  The shift
+// amounts the MAC needs are read from two small shared-memory tables indexed
+// by E (one LDS.64 each) instead of being recomputed with ALU ops:
+//   product: Tp[E] = { t + 2 (bits of hi below the kept fraction, + n), t + 3 }
+//   sum:     Tx[E] = { t + 4 (+ BAD_FLAG if t > 26), t + 3 }
+constexpr int TBIAS = 160;               // table index = E + TBIAS, E in [-160, 223]
+constexpr int TSIZE = 384;
+constexpr uint32_t BAD_FLAG = 1u << 23;  // accumulated with IMAD; checked once per k-slab
+constexpr int E_CLAMP = 150;             // accumulator scales are clamped per k-slab (table bounds)
+
+__device__ __forceinline__ void fill_tables(uint2* tp, uint2* tx, int tid, int nthr) {
+  for (int i = tid; i < TSIZE; i += nthr) {
+    const int E = i - TBIAS;
+    const uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
+    tp[i] = make_uint2(t + 2u, t + 3u);
+    tx[i] = make_uint2(t + 4u + (t > (uint32_t)T_FAST_MAX ? BAD_FLAG : 0u), t + 3u);
+  }
+}
+
 // ---- the decoded-domain MAC -------------------------------------------------
 // c <- c (+) (a (x) b), a = (Ma hidden@31, wa), b = (Mb hidden@30, wb).
-// bad |= the fast path cannot represent the result (caller recomputes).
-__device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t Mb, uint32_t wb, bool& bad) {
+// tp / tx point at table entry E = 0.  badacc accumulates BAD_FLAG when the
+// sum leaves the fast range (the caller checks it once per k-slab).
+__device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t Mb, uint32_t wb, const uint2* tp,
+                                    const uint2* tx, uint32_t& badacc) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
   const uint32_t wab = wa + wb;                       // (Ea+Eb) << 8 | (sa + sb)
   const uint32_t hi = __umulhi(Ma, Mb);               // [2^29, 2^31)
   const uint32_t lo = Ma * Mb;                        // sticky source
   const uint32_t n = hi >> 30;
   const int32_t Ep = ((int32_t)wab >> 8) + (int32_t)n;
-  const uint32_t tp = (uint32_t)(Ep ^ (Ep >> 31)) >> 2;
-  const uint32_t Dp = tp + n + 2;                     // bits of hi below the kept fraction
+  const uint2 T = tp[Ep];
+  const uint32_t Dp = T.x + n;                        // bits of hi below the kept fraction
   const uint32_t qp = hi >> Dp;
   const uint32_t yp = __funnelshift_r(0u, hi, Dp) | (qp & 1u);   // dropped bits at top, lsb at bit 0
   uint32_t rp;
@@ -98,8 +123,8 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t M
       "addc.cc.u32 t, %2, 0x7FFFFFFF;\n\t"            // CF = round up (RNE)
       "addc.u32 %0, %3, 0;\n\t}"
       : "=r"(rp) : "r"(lo), "r"(yp), "r"(qp));
-  const uint32_t Mp = rp << (tp + 3);                 // hidden@30 (2^31 if rounding carried)
-  const uint32_t sp = wab & 1u;
+  const uint32_t Mp = rp << T.y;                      // hidden@30 (2^31 if rounding carried)
+  // sign of the product = bit 0 of wab (sa + sb); c.s keeps its sign in bit 0 too
 
   // -- sum: exact aligned add with jammed sticky, rounded once at f_s(Ex) --
   // lexicographic (E, M) compare as one 64-bit signed compare: branch-free
@@ -107,33 +132,34 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t M
   const long long kc = (long long)(((unsigned long long)(uint32_t)c.E << 32) | c.M);
   const bool pbig = kp > kc;
   const uint32_t Mbg = pbig ? Mp : c.M;
-  const uint32_t Msm = pbig ? c.M : Mp;
-  const uint32_t sbg = pbig ? sp : c.s;
-  const int32_t Ebg = pbig ? Ep : c.E;
-  const uint32_t ad = (uint32_t)abs(Ep - c.E);
+  const uint32_t Msm = (Mp + c.M) - Mbg;
+  const uint32_t sbg = pbig ? wab : c.s;
+  const int32_t Ebg = max(Ep, c.E);
+  const uint32_t ad = (uint32_t)(2 * Ebg - (Ep + c.E));        // |Ep - Ec|
   const uint32_t sh = __funnelshift_rc(Msm, 0u, ad);          // Msm >> min(ad, 32)
   const uint32_t lost = __funnelshift_rc(0u, Msm, ad);        // bits shifted out (nonzero iff any)
   const uint32_t Msj = sh | min(lost, 1u);                    // jam sticky into bit 0
-  const uint32_t eff = sp ^ c.s;                              // effective subtraction
+  const uint32_t eff = (wab ^ c.s) & 1u;                      // effective subtraction
   const uint32_t x = Mbg + (Msj ^ (0u - eff)) + eff;          // |big| +/- |small|, >= 0
   const int lz = __clz((int)x);
   const uint32_t xn = __funnelshift_lc(0u, x, lz);           // x << lz: leading one at 31 (0 if x == 0)
   const int32_t Ex = Ebg + 1 - lz;
-  const uint32_t tx = (uint32_t)(Ex ^ (Ex >> 31)) >> 2;
-  const uint32_t Dx = tx + 4;
-  const uint32_t qx = xn >> Dx;
-  const uint32_t yx = __funnelshift_r(0u, xn, Dx) | (qx & 1u);
+  const uint2 U = tx[Ex];
+  const uint32_t qx = __funnelshift_r(xn, 0u, U.x);          // xn >> (U.x & 31)
+  const uint32_t yx = __funnelshift_r(0u, xn, U.x) | (qx & 1u);
   uint32_t rx;
   asm("{\n\t.reg .u32 t;\n\t"
       "add.cc.u32 t, %1, 0x7FFFFFFF;\n\t"
       "addc.u32 %0, %2, 0;\n\t}"
       : "=r"(rx) : "r"(yx), "r"(qx));
-  uint32_t Mn = rx << (tx + 3);                               // hidden@30, or 2^31 on carry
+  const uint32_t Mn = rx << U.y;                              // hidden@30, or 2^31 on carry
   const uint32_t cy = Mn >> 31;
   c.M = Mn >> cy;
-  c.E = Ex + (int32_t)cy;
+  // exact cancellation (x == 0): xn's top bit is clear -> scale far below any
+  // product, so the zero accumulator is the small operand of the next add
+  c.E = (int32_t)(xn >> 31) * 4096 + (Ex + (int32_t)cy - 4096);
   c.s = sbg;
-  bad = bad | (tx > (uint32_t)T_FAST_MAX) | (x == 0u);
+  badacc += U.x;                                              // BAD_FLAG bits accumulate
 }
 
 }  // namespace pg

@@ -26,7 +26,13 @@ __global__ void kern(unsigned* out, unsigned seed, long long* cyc) {
       if (OP == 7) { if (i & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
                      else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[i]) : "r"(b), "r"(c)); }
       if (OP == 8) asm volatile("add.cc.u32 %0, %0, %1; addc.u32 %0, %0, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
-      if (OP == 9) asm volatile("setp.gt.u32 %%p1, %0, %1;" :: "r"(r[i]), "r"(b));
+      if (OP == 9) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 10) { double d = __longlong_as_double(((long long)r[i] << 20) | 0x3FF0000000000000ll);
+                      asm volatile("fma.rn.f64 %0, %0, %0, %0;" : "+d"(d)); r[i] = (unsigned)__double_as_longlong(d); }
+      if (OP == 11) asm volatile("add.u32 %0, %0, %1; add.u32 %0, %0, %2;" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 12) asm volatile("shr.u32 %0, %0, 3; add.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(b));
+      if (OP == 13) asm volatile("min.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(b));
+      if (OP == 14) asm volatile("abs.s32 %0, %0;" : "+r"(r[i]));
     }
   }
   long long t1 = clock64();
@@ -62,7 +68,12 @@ int main() {
   run<5>("bfind (FLO)", 1, out, cyc, nsm, false);
   run<6>("setp+selp (ISETP+SEL)", 2, out, cyc, nsm, false);
   run<7>("mad.lo/lop3 mix", 1, out, cyc, nsm, false);
-  run<8>("add.cc+addc", 2, out, cyc, nsm, true);
+  run<8>("add.cc+addc", 2, out, cyc, nsm, false);
+  run<9>("fma.f32 (FFMA)", 1, out, cyc, nsm, false);
+  run<11>("add+add 3-operand", 2, out, cyc, nsm, false);
+  run<12>("shr+add (LEA.HI)", 2, out, cyc, nsm, false);
+  run<13>("min.u32 (IMNMX)", 1, out, cyc, nsm, false);
+  run<14>("abs (IABS)", 1, out, cyc, nsm, true);
   printf("}\n");
   return 0;
 }
