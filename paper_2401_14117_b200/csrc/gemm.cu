@@ -22,7 +22,7 @@ struct Cfg {
     uint2 a[2][BK][BM];
     uint2 b[2][BK][BN];
     uint2 tp[TSIZE];
-    uint2 tx[TSIZE];
+    uint4 tx[TSIZE];
   };
 };
 
@@ -83,8 +83,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 
   const uint32_t flip = P.neg ? 1u : 0u;
   fill_tables(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
-  const uint2* tabp = S.tp + TBIAS;
-  const uint2* tabx = S.tx + TBIAS;
+  MacConst K;
+  K.one = (uint32_t)P.one; K.two = 2u * K.one; K.eight = 8u * K.one; K.sixteen = 16u * K.one;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + TBIAS) - 30u * 16u;   // indexed by Ex + 30
 
   // ---- accumulators -------------------------------------------------------
   Acc acc[TM][TN];
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, tabp, tabx, badacc);
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, K, badacc);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, tabp, tabx, badacc);
+            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, K, badacc);
         }
       }
       // once per k-slab: fold the accumulated flags, bound the scales (table range)

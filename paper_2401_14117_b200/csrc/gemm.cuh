@@ -43,6 +43,7 @@ struct Params {
   int neg;        // alpha = -1
   int beta;       // 0 or 1
   const int32_t* stop;   // optional device flag: nonzero -> the kernel is a no-op (potrf after a failure)
+  int one = 1;           // the constant 1, passed at run time (keeps IMADs on the FMA pipe)
 };
 
 // ---- staging decode --------------------------------------------------------
@@ -67,7 +68,7 @@ __device__ __forceinline__ uint2 stage_decode(uint32_t x, uint32_t flip, uint32_
 struct Acc { uint32_t M; int32_t E; uint32_t s; };
 
 __device__ __forceinline__ uint32_t acc_encode(const Acc& c) {
-  if (c.M == 0u) return 0u;
+  if (c.M == 0u || c.E < -1000) return 0u;          // exact zero (see mac: scale far below range)
   // M hidden at 30 -> S hidden at 63; the sign is bit 0 of c.s
   return p32::round_encode(c.s & 1u, c.E, (uint64_t)c.M << 33);
 }
@@ -84,37 +85,66 @@ __device__ __forceinline__ bool acc_decode(uint32_t x, Acc& c) {
 // For a scale E the posit fraction width is f_s(E) = 27 - t(E) with
 // t(E) = (E ^ (E >> 31)) >> 2 (valid for |E| <= 107, f_s >= 1).  The shift
 // amounts the MAC needs are read from two small shared-memory tables indexed
-// by E (one LDS.64 each) instead of being recomputed with ALU ops:
+// by E (one LDS each) instead of being recomputed with ALU ops:
 //   product: Tp[E] = { t + 2 (bits of hi below the kept fraction, + n), t + 3 }
-//   sum:     Tx[E] = { t + 4 (+ BAD_FLAG if t > 26), t + 3 }
-constexpr int TBIAS = 160;               // table index = E + TBIAS, E in [-160, 223]
+//   sum:     Tx[E] = { t + 5 (+ BAD_FLAG if t > 26), t + 3, 2^(27 - t), 0 }
+// (the sum rounds the 32 fraction bits only, keeping f_s = 27 - t of them;
+//  the hidden bit 2^(27-t) in units of the kept fraction lsb is added
+//  back inside the rounding carry chain).
+constexpr int TBIAS = 192;               // table index = E + TBIAS, E in [-192, 191]
 constexpr int TSIZE = 384;
 constexpr uint32_t BAD_FLAG = 1u << 23;  // accumulated with IMAD; checked once per k-slab
 constexpr int E_CLAMP = 150;             // accumulator scales are clamped per k-slab (table bounds)
+constexpr int E_ZERO_LIMIT = -1000;      // scales below this encode an exact zero accumulator
 
-__device__ __forceinline__ void fill_tables(uint2* tp, uint2* tx, int tid, int nthr) {
+__device__ __forceinline__ void fill_tables(uint2* tp, uint4* tx, int tid, int nthr) {
   for (int i = tid; i < TSIZE; i += nthr) {
     const int E = i - TBIAS;
     const uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     tp[i] = make_uint2(t + 2u, t + 3u);
-    tx[i] = make_uint2(t + 4u + (t > (uint32_t)T_FAST_MAX ? BAD_FLAG : 0u), t + 3u);
+    const bool fast = t <= (uint32_t)T_FAST_MAX;
+    tx[i] = make_uint4(t + 5u + (fast ? 0u : BAD_FLAG), t + 3u, fast ? (1u << (27 - t)) : 0u, 0u);
   }
 }
 
+// integer multiply-add forced onto the FMA pipe (the ALU pipe is the bottleneck):
+// the multiplier comes from a kernel parameter, so ptxas cannot strength-reduce it.
+__device__ __forceinline__ uint32_t fmad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+struct MacConst {
+  uint32_t one, two, eight, sixteen;   // = 1, 2, 8, 16 at run time (opaque to ptxas)
+  uint32_t tp0, tx0;                   // shared-memory byte addresses of table entry E = 0
+};
+
 // ---- the decoded-domain MAC -------------------------------------------------
 // c <- c (+) (a (x) b), a = (Ma hidden@31, wa), b = (Mb hidden@30, wb).
-// tp / tx point at table entry E = 0.  badacc accumulates BAD_FLAG when the
-// sum leaves the fast range (the caller checks it once per k-slab).
-__device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t Mb, uint32_t wb, const uint2* tp,
-                                    const uint2* tx, uint32_t& badacc) {
+// badacc accumulates BAD_FLAG when the sum leaves the fast range (the caller
+// checks it once per k-slab).
+__device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t Mb, uint32_t wb, const MacConst& K,
+                                    uint32_t& badacc) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
-  const uint32_t wab = wa + wb;                       // (Ea+Eb) << 8 | (sa + sb)
+  const uint32_t wab = fmad(wa, K.one, wb);           // (Ea+Eb) << 8 | (sa + sb)
   const uint32_t hi = __umulhi(Ma, Mb);               // [2^29, 2^31)
   const uint32_t lo = Ma * Mb;                        // sticky source
   const uint32_t n = hi >> 30;
   const int32_t Ep = ((int32_t)wab >> 8) + (int32_t)n;
-  const uint2 T = tp[Ep];
-  const uint32_t Dp = T.x + n;                        // bits of hi below the kept fraction
+  const uint2 T = lds64(fmad((uint32_t)Ep, K.eight, K.tp0));
+  const uint32_t Dp = fmad(n, K.one, T.x);            // bits of hi below the kept fraction
   const uint32_t qp = hi >> Dp;
   const uint32_t yp = __funnelshift_r(0u, hi, Dp) | (qp & 1u);   // dropped bits at top, lsb at bit 0
   uint32_t rp;
@@ -132,34 +162,38 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, uint32_t wa, uint32_t M
   const long long kc = (long long)(((unsigned long long)(uint32_t)c.E << 32) | c.M);
   const bool pbig = kp > kc;
   const uint32_t Mbg = pbig ? Mp : c.M;
-  const uint32_t Msm = (Mp + c.M) - Mbg;
+  const uint32_t Msm = fmad(Mbg, 0u - K.one, fmad(Mp, K.one, c.M));        // the other one
   const uint32_t sbg = pbig ? wab : c.s;
   const int32_t Ebg = max(Ep, c.E);
-  const uint32_t ad = (uint32_t)(2 * Ebg - (Ep + c.E));        // |Ep - Ec|
+  const uint32_t ad = fmad((uint32_t)Ebg, K.two, 0u - fmad((uint32_t)Ep, K.one, (uint32_t)c.E));  // |Ep - Ec|
   const uint32_t sh = __funnelshift_rc(Msm, 0u, ad);          // Msm >> min(ad, 32)
   const uint32_t lost = __funnelshift_rc(0u, Msm, ad);        // bits shifted out (nonzero iff any)
-  const uint32_t Msj = sh | min(lost, 1u);                    // jam sticky into bit 0
+  uint32_t jam;
+  asm("min.u32 %0, %1, 1;" : "=r"(jam) : "r"(lost));          // sticky of the shifted-out bits
+  const uint32_t Msj = sh | jam;                              // jam sticky into bit 0
   const uint32_t eff = (wab ^ c.s) & 1u;                      // effective subtraction
   const uint32_t x = Mbg + (Msj ^ (0u - eff)) + eff;          // |big| +/- |small|, >= 0
-  const int lz = __clz((int)x);
-  const uint32_t xn = __funnelshift_lc(0u, x, lz);           // x << lz: leading one at 31 (0 if x == 0)
-  const int32_t Ex = Ebg + 1 - lz;
-  const uint2 U = tx[Ex];
-  const uint32_t qx = __funnelshift_r(xn, 0u, U.x);          // xn >> (U.x & 31)
-  const uint32_t yx = __funnelshift_r(0u, xn, U.x) | (qx & 1u);
+  uint32_t flo;
+  asm("bfind.u32 %0, %1;" : "=r"(flo) : "r"(x));             // leading one (0xFFFFFFFF if x == 0)
+  const uint32_t xf = __funnelshift_r(0u, x, flo);            // fraction bits left-aligned (hidden dropped)
+  const uint32_t Exi = fmad(flo, K.one, (uint32_t)Ebg);       // Ex + 30
+  const uint4 U = lds128(fmad(Exi, K.sixteen, K.tx0));
+  const uint32_t qx = __funnelshift_r(xf, 0u, U.x);          // xf >> (U.x & 31)
+  const uint32_t yx = __funnelshift_r(0u, xf, U.x) | (qx & 1u);
   uint32_t rx;
   asm("{\n\t.reg .u32 t;\n\t"
       "add.cc.u32 t, %1, 0x7FFFFFFF;\n\t"
-      "addc.u32 %0, %2, 0;\n\t}"
-      : "=r"(rx) : "r"(yx), "r"(qx));
+      "addc.u32 %0, %2, %3;\n\t}"                      // + hidden bit + round up
+      : "=r"(rx) : "r"(yx), "r"(qx), "r"(U.z));
   const uint32_t Mn = rx << U.y;                              // hidden@30, or 2^31 on carry
   const uint32_t cy = Mn >> 31;
   c.M = Mn >> cy;
-  // exact cancellation (x == 0): xn's top bit is clear -> scale far below any
-  // product, so the zero accumulator is the small operand of the next add
-  c.E = (int32_t)(xn >> 31) * 4096 + (Ex + (int32_t)cy - 4096);
+  // exact cancellation (x == 0, flo = -1): scale pushed far below any product,
+  // so the (zero) accumulator is the small operand of every later add
+  const int32_t E1 = (int32_t)Exi + (int32_t)cy - 30;
+  c.E = (int32_t)fmad((uint32_t)((int32_t)flo >> 31), 4096u, (uint32_t)E1);
   c.s = sbg;
-  badacc += U.x;                                              // BAD_FLAG bits accumulate
+  badacc = fmad(U.x, K.one, badacc);                          // BAD_FLAG bits accumulate
 }
 
 }  // namespace pg
