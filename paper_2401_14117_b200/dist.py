@@ -1,0 +1,169 @@
+"""Multi-GPU Posit(32,2) LU: 1 x P column-block-cyclic layout, NCCL panel broadcast.
+
+BASELINE.json north_star (3): "the trailing update is split by column blocks,
+2D block-cyclic, with NCCL broadcast of the factored panel and pivot rows over
+NVLink".  SURVEY.md 8(e).  The paper itself drives one accelerator over PCIe
+(P:435-436); this layer is B200-first, not a port.
+
+Layout.  The n x n matrix is cut into column blocks of nb; rank r of P owns
+the blocks j with j mod P == r, stored side by side (ascending j) in one local
+row-major n x (nloc) tensor -- all rows, its own columns.
+
+Per panel step s (columns [s nb, s nb + b)), owner o = s mod P:
+  1. owner: unblocked LU of its (n - s nb) x b panel in place (posit_getrf_panel:
+     pivot by signed-int compare, swap inside the panel, posit division,
+     in-panel update), ipiv in global 1-based rows;
+  2. owner packs [panel | ipiv | info] into one int32 buffer; ONE broadcast
+     (torch.distributed -> ncclBroadcast over NVLink / NVSwitch);
+  3. every rank: laswp of the step's b interchanges on all its other columns,
+     U12 = L11^-1 A12 (unit-lower TRSM) and A22 <- A22 - L21 U12 (the hot GEMM)
+     on its columns right of the panel.
+No reductions in the data path.  By the order contract (Q6) every
+element still receives its products one at a time in ascending k, so the
+factors are bit-identical to the single-GPU posit_getrf and to the textbook
+loop for every P.
+
+The arithmetic goes through an ``ops`` object.  The product uses ``CudaOps``
+(the C ABI of libposit_b200.so on the current CUDA stream); the CPU tests pass
+their own implementation of the same five calls to exercise this schedule on
+``gloo`` without a GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class BlockCyclic1D:
+    """Column-block-cyclic descriptor: n x n matrix, blocks of nb columns over P ranks."""
+    n: int
+    nb: int
+    nprocs: int
+    rank: int
+
+    @property
+    def nblocks(self) -> int:
+        return (self.n + self.nb - 1) // self.nb
+
+    def owner(self, j: int) -> int:
+        return j % self.nprocs
+
+    def block_width(self, j: int) -> int:
+        return min(self.nb, self.n - j * self.nb)
+
+    def local_blocks(self, rank: int | None = None) -> list[int]:
+        r = self.rank if rank is None else rank
+        return list(range(r, self.nblocks, self.nprocs))
+
+    def local_cols(self, rank: int | None = None) -> int:
+        return sum(self.block_width(j) for j in self.local_blocks(rank))
+
+    def local_offset(self, j: int) -> int:
+        """Column offset of global block j inside its owner's local storage."""
+        return sum(self.block_width(i) for i in range(self.owner(j), j, self.nprocs))
+
+    def first_local_after(self, s: int, rank: int | None = None) -> int:
+        """Local column offset of this rank's first block with global index > s
+        (== local_cols() if none)."""
+        off = 0
+        for j in self.local_blocks(rank):
+            if j > s:
+                return off
+            off += self.block_width(j)
+        return off
+
+    def scatter(self, A: torch.Tensor, rank: int | None = None) -> torch.Tensor:
+        """This rank's local columns of the full matrix A (a copy)."""
+        cols = [A[:, j * self.nb: j * self.nb + self.block_width(j)] for j in self.local_blocks(rank)]
+        if not cols:
+            return A.new_empty((self.n, 0))
+        return torch.cat(cols, dim=1).contiguous()
+
+    def gather(self, locals_by_rank: list[torch.Tensor]) -> torch.Tensor:
+        """Reassemble the full matrix from every rank's local tensor."""
+        out = locals_by_rank[0].new_empty((self.n, self.n))
+        for r, L in enumerate(locals_by_rank):
+            off = 0
+            for j in self.local_blocks(r):
+                w = self.block_width(j)
+                out[:, j * self.nb: j * self.nb + w] = L[:, off: off + w]
+                off += w
+        return out
+
+
+class CudaOps:
+    """The product arithmetic: libposit_b200.so through the package binding."""
+
+    def __init__(self):
+        import paper_2401_14117_b200 as PB
+        self.PB = PB
+
+    def getrf_panel(self, P, ipiv, info, row_base):
+        self.PB.posit_getrf_panel(P, ipiv, info, row_base=row_base)
+
+    def laswp(self, A, k1, k2, ipiv):
+        if A.shape[1] > 0:
+            self.PB.posit_laswp(A, k1, k2, ipiv, ipiv_base=0)
+
+    def trsm_llnu(self, L, B):
+        if B.shape[1] > 0:
+            self.PB.posit_trsm("L", "L", "N", "U", L, B)
+
+    def gemm_minus(self, A, B, C):
+        if C.shape[0] > 0 and C.shape[1] > 0:
+            self.PB.posit_gemm(A, B, C)
+
+
+def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, info: torch.Tensor,
+               ops=None, group=None) -> None:
+    """In-place distributed LU with partial pivoting of the n x n matrix whose
+    local columns (desc.scatter) are A_local (int32 pattern storage, row-major).
+
+    ipiv (int32, n) receives the global 1-based pivots on EVERY rank; info
+    (int32, 1) the first zero-pivot column (1-based) or 0, on every rank.
+    """
+    ops = CudaOps() if ops is None else ops
+    n, nb, P, me = desc.n, desc.nb, desc.nprocs, desc.rank
+    if A_local.shape != (n, desc.local_cols()):
+        raise ValueError(f"A_local has shape {tuple(A_local.shape)}, expected {(n, desc.local_cols())}")
+    dev = A_local.device
+    info.zero_()
+    my_info = torch.zeros(1, dtype=torch.int32, device=dev)
+    nloc = A_local.shape[1]
+    for s in range(desc.nblocks):
+        r0 = s * nb
+        b = desc.block_width(s)
+        m = n - r0
+        o = desc.owner(s)
+        buf = torch.empty(m * b + b + 1, dtype=torch.int32, device=dev)
+        panel = buf[: m * b].view(m, b)
+        if me == o:
+            lc = desc.local_offset(s)
+            Ap = A_local[r0:, lc: lc + b]
+            ops.getrf_panel(Ap, ipiv[r0: r0 + b], my_info, r0)
+            panel.copy_(Ap)
+            buf[m * b: m * b + b].copy_(ipiv[r0: r0 + b])
+            buf[m * b + b: m * b + b + 1].copy_(my_info)
+        if P > 1:
+            dist.broadcast(buf, src=o, group=group)
+        if me != o:
+            ipiv[r0: r0 + b].copy_(buf[m * b: m * b + b])
+        # first zero pivot so far, identical on every rank (the owner's counter is cumulative)
+        step_info = buf[m * b + b: m * b + b + 1]
+        info.copy_(torch.where(info != 0, info, step_info))
+        # 3. interchanges on every local column outside this panel
+        if me == o:
+            lc = desc.local_offset(s)
+            ops.laswp(A_local[:, :lc], r0, r0 + b, ipiv)
+            ops.laswp(A_local[:, lc + b:], r0, r0 + b, ipiv)
+        else:
+            ops.laswp(A_local, r0, r0 + b, ipiv)
+        # 4. U12 and the trailing update on the columns right of the panel
+        t0 = desc.first_local_after(s)
+        if t0 < nloc and r0 + b <= n:
+            ops.trsm_llnu(panel[:b], A_local[r0: r0 + b, t0:])
+            if r0 + b < n:
+                ops.gemm_minus(panel[b:], A_local[r0: r0 + b, t0:], A_local[r0 + b:, t0:])

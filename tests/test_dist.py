@@ -1,0 +1,117 @@
+"""The multi-GPU LU schedule (paper_2401_14117_b200/dist.py) on CPU: gloo
+process groups of world size 2 and 3, the arithmetic supplied by the oracle
+(test infrastructure) through the same five-call ``ops`` interface the CUDA
+path implements.  The gathered factors, ipiv and info must equal the textbook
+unblocked oracle LU bit for bit (Q6: distribution is a traversal
+change only), for every P.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synthetic_inputs as SI
+from oracle import oracle as O
+from paper_2401_14117_b200.dist import BlockCyclic1D, getrf_dist
+
+
+def _np(t):
+    return t.contiguous().numpy().view(np.uint32)
+
+
+class OracleOps:
+    """CPU stand-in for CudaOps (tests only)."""
+
+    def getrf_panel(self, P, ipiv, info, row_base):
+        lu, piv, inf = O.getrf(_np(P))
+        P.copy_(torch.from_numpy(lu.view(np.int32)))
+        ipiv.copy_(torch.from_numpy(piv + row_base))
+        if int(info[0]) == 0 and inf != 0:
+            info[0] = inf + row_base
+
+    def laswp(self, A, k1, k2, ipiv):
+        for k in range(k1, k2):
+            p = int(ipiv[k]) - 1
+            if p != k:
+                t = A[k].clone()
+                A[k] = A[p]
+                A[p] = t
+
+    def trsm_llnu(self, L, B):
+        if B.shape[1]:
+            B.copy_(torch.from_numpy(O.trsm_llnu(_np(L), _np(B)).view(np.int32)))
+
+    def gemm_minus(self, A, B, C):
+        if C.shape[0] and C.shape[1]:
+            C.copy_(torch.from_numpy(O.gemm(_np(A), _np(B), _np(C)).view(np.int32)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, A, nb, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = A.shape[0]
+        desc = BlockCyclic1D(n, nb, world, rank)
+        full = torch.from_numpy(A.view(np.int32))
+        loc = desc.scatter(full)
+        ipiv = torch.zeros(n, dtype=torch.int32)
+        info = torch.zeros(1, dtype=torch.int32)
+        getrf_dist(loc, desc, ipiv, info, ops=OracleOps())
+        out[rank] = (loc.numpy().copy(), ipiv.numpy().copy(), int(info[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(A, nb, world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), A, nb, out), nprocs=world, join=True)
+    n = A.shape[0]
+    desc = BlockCyclic1D(n, nb, world, 0)
+    full = desc.gather([torch.from_numpy(out[r][0]) for r in range(world)]).numpy().view(np.uint32)
+    return full, [out[r][1] for r in range(world)], [out[r][2] for r in range(world)]
+
+
+def test_block_cyclic_descriptor():
+    d = BlockCyclic1D(100, 16, 3, 1)
+    assert d.nblocks == 7 and d.local_blocks() == [1, 4] and d.local_cols() == 32
+    assert BlockCyclic1D(100, 16, 3, 0).local_cols() == 16 + 16 + 4     # blocks 0, 3, 6 (ragged)
+    assert d.local_offset(4) == 16 and d.first_local_after(1) == 16 and d.first_local_after(4) == 32
+    A = torch.arange(100 * 100, dtype=torch.int32).view(100, 100)
+    parts = [BlockCyclic1D(100, 16, 3, r).scatter(A) for r in range(3)]
+    assert torch.equal(d.gather(parts), A)
+
+
+@pytest.mark.parametrize("world,n,nb", [(2, 80, 16), (3, 70, 8)])
+def test_getrf_dist_gloo_matches_oracle(world, n, nb):
+    A = O.from_f64_array(SI.config4(n))           # configs[3] recipe (U[-1,1), seed 3) at small n
+    full, pivs, infos = _run(A, nb, world)
+    ref, rpiv, rinfo = O.getrf(A)
+    assert int(np.count_nonzero(full != ref)) == 0
+    for p, i in zip(pivs, infos):
+        assert np.array_equal(p, rpiv) and i == rinfo
+
+
+def test_getrf_dist_gloo_zero_pivot_info():
+    # a rank-deficient matrix: column 20 equals column 3 -> an exact zero pivot appears
+    n, nb = 48, 8
+    A64 = SI.config4(n)
+    A64[:, 20] = 0.0
+    A = O.from_f64_array(A64)
+    full, pivs, infos = _run(A, nb, 2)
+    ref, rpiv, rinfo = O.getrf(A)
+    assert rinfo == 21
+    assert int(np.count_nonzero(full != ref)) == 0 and all(i == rinfo for i in infos)
