@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define POSIT_ABI_VERSION 1
+#define POSIT_ABI_VERSION 2
 #define POSIT_OK 0
 #define POSIT_ENOTSUP (-100)
 #define POSIT_ECUDA (-101)
@@ -55,6 +55,10 @@ extern "C" {
 
 /* Library version (POSIT_ABI_VERSION). */
 int posit_abi_version(void);
+
+/* Number of CUDA kernels this library has launched in this process so far
+ * (all entry points, all threads; a monotone counter for launch accounting). */
+uint64_t posit_kernel_launches(void);
 
 /* Static description of a return code. */
 const char* posit_strerror(int code);
@@ -127,7 +131,9 @@ int posit_trsm(char side, char uplo, char transa, char diag, int64_t m, int64_t 
  * (one posit division, Q8) for i > k, else *info = first such k+1 (Q11, the
  * factorisation continues); a_ij <- a_ij (-) a_ik (x) a_kj for i,j > k.
  * On exit A holds L (unit, strictly lower) and U; ipiv (length min(m,n)) and
- * info are DEVICE int32.  work may be NULL when posit_getrf_work_bytes() == 0.
+ * info are DEVICE int32.  work is a DEVICE workspace of at least
+ * posit_getrf_work_bytes(m, n, nb) bytes (pivot keys of the panel), owned by
+ * the caller and not used concurrently by another call (else -8).
  */
 size_t posit_getrf_work_bytes(int64_t m, int64_t n, int64_t nb);
 int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t nb,
@@ -138,10 +144,11 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
  * A (the panel step of posit_getrf; used by the multi-GPU driver).  Row swaps
  * are applied inside the panel only.  ipiv[j] receives row_base + p + 1
  * (1-based, offset by row_base); *info, if still 0, receives row_base + j + 1
- * at the first zero pivot.
+ * at the first zero pivot.  work: DEVICE workspace of posit_getrf_work_bytes()
+ * bytes (else -8).
  */
 int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
-                      int64_t row_base, void* stream);
+                      int64_t row_base, void* work, size_t work_bytes, void* stream);
 
 /*
  * posit_laswp -- apply the row interchanges ipiv[k1..k2) in order to columns

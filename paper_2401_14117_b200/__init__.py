@@ -19,7 +19,7 @@ import os
 __all__ = [
     "lib", "PositError", "posit_gemm", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
     "posit_getrf", "posit_getrf_panel", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
-    "posit_vec_op", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
+    "posit_vec_op", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
 ]
 
 POSIT_ONE = 0x40000000
@@ -55,7 +55,7 @@ def lib() -> ctypes.CDLL:
         L.posit_getrf.argtypes = [i64, i64, vp, i64, vp, vp, i64, vp, sz, vp]
         L.posit_getrf_work_bytes.argtypes = [i64, i64, i64]
         L.posit_getrf_work_bytes.restype = sz
-        L.posit_getrf_panel.argtypes = [i64, i64, vp, i64, vp, vp, i64, vp]
+        L.posit_getrf_panel.argtypes = [i64, i64, vp, i64, vp, vp, i64, vp, sz, vp]
         L.posit_laswp.argtypes = [i64, vp, i64, i64, i64, vp, i64, vp]
         L.posit_potrf.argtypes = [c_char, i64, vp, i64, vp, i64, vp, sz, vp]
         L.posit_potrf_work_bytes.argtypes = [i64, i64]
@@ -63,11 +63,17 @@ def lib() -> ctypes.CDLL:
         L.posit_from_f64.argtypes = [vp, vp, i64, vp]
         L.posit_to_f64.argtypes = [vp, vp, i64, vp]
         L.posit_vec_op.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp]
+        L.posit_kernel_launches.restype = ctypes.c_uint64
         L.posit_strerror.argtypes = [ctypes.c_int]
         L.posit_strerror.restype = ctypes.c_char_p
         L.posit_last_error.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def posit_kernel_launches() -> int:
+    """Kernels launched by libposit_b200 in this process so far."""
+    return int(lib().posit_kernel_launches())
 
 
 def _check(rc: int, name: str) -> None:
@@ -141,17 +147,27 @@ def posit_trsm(side: str, uplo: str, transa: str, diag: str, A, B, stream=None) 
                             _ld(A), _ptr(B), _ld(B), _stream(stream)), "posit_trsm")
 
 
-def posit_getrf(A, ipiv, info, nb: int = 256, stream=None) -> None:
-    """In-place blocked LU with partial pivoting; ipiv (int32, min(m,n)) and info (int32, 1) are device tensors."""
+def _work(nbytes: int, like, work):
+    import torch
+    if work is None:
+        work = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=like.device)
+    return work, work.numel() * work.element_size()
+
+
+def posit_getrf(A, ipiv, info, nb: int = 256, stream=None, work=None) -> None:
+    """In-place blocked LU with partial pivoting; ipiv (int32, min(m,n)) and info (int32, 1) are device tensors.
+    work: optional device byte tensor of posit_getrf_work_bytes() bytes (allocated here if None)."""
     m, n = A.shape
-    _check(lib().posit_getrf(m, n, _ptr(A), _ld(A), _ptr(ipiv), _ptr(info), nb, None, 0, _stream(stream)),
+    w, wb = _work(int(lib().posit_getrf_work_bytes(m, n, nb)), A, work)
+    _check(lib().posit_getrf(m, n, _ptr(A), _ld(A), _ptr(ipiv), _ptr(info), nb, _ptr(w), wb, _stream(stream)),
            "posit_getrf")
 
 
-def posit_getrf_panel(P, ipiv, info, row_base: int = 0, stream=None) -> None:
+def posit_getrf_panel(P, ipiv, info, row_base: int = 0, stream=None, work=None) -> None:
     m, b = P.shape
-    _check(lib().posit_getrf_panel(m, b, _ptr(P), _ld(P), _ptr(ipiv), _ptr(info), row_base, _stream(stream)),
-           "posit_getrf_panel")
+    w, wb = _work(int(lib().posit_getrf_work_bytes(m, b, b)), P, work)
+    _check(lib().posit_getrf_panel(m, b, _ptr(P), _ld(P), _ptr(ipiv), _ptr(info), row_base, _ptr(w), wb,
+                                   _stream(stream)), "posit_getrf_panel")
 
 
 def posit_laswp(A, k1: int, k2: int, ipiv, ipiv_base: int = 0, stream=None) -> None:

@@ -3,10 +3,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <atomic>
 #include "gemm.cuh"
 #include "internal.h"
 
 static thread_local char g_last_error[256] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void pb_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static int cuda_check(cudaError_t e) {
   if (e == cudaSuccess) return 0;
@@ -27,6 +31,8 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 extern "C" {
 
 int posit_abi_version(void) { return POSIT_ABI_VERSION; }
+
+uint64_t posit_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* posit_strerror(int code) {
   if (code == POSIT_OK) return "ok";
@@ -156,16 +162,17 @@ int posit_trsm(char side, char uplo, char transa, char diag, int64_t m, int64_t 
 
 size_t posit_getrf_work_bytes(int64_t m, int64_t n, int64_t nb) {
   (void)m; (void)n; (void)nb;
-  return 0;
+  return pb_panel_ws_bytes();
 }
 
 int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
-                      void* stream) {
+                      void* work, size_t work_bytes, void* stream) {
   if (m < 0) return -1;
   if (b < 0) return -2;
   if (lda < (b > 1 ? b : 1)) return -4;
   if (m == 0 || b == 0) return 0;
-  return launch_check(pb_getrf_panel(m, b, A, lda, ipiv, info, row_base, nullptr, S(stream)));
+  if (work == nullptr || work_bytes < pb_panel_ws_bytes()) return -8;
+  return launch_check(pb_getrf_panel(m, b, A, lda, ipiv, info, row_base, work, S(stream)));
 }
 
 int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
@@ -178,12 +185,12 @@ int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2,
 
 int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t nb,
                 void* work, size_t work_bytes, void* stream) {
-  (void)work; (void)work_bytes;
   if (m < 0) return -1;
   if (n < 0) return -2;
   if (lda < (n > 1 ? n : 1)) return -4;
   if (nb < 1) return -7;
   if (info == nullptr) return -6;
+  if (work == nullptr || work_bytes < pb_panel_ws_bytes()) return -8;
   cudaStream_t st = S(stream);
   int rc = cuda_check(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   if (rc) return rc;
@@ -191,7 +198,7 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
   for (int64_t s = 0; s < kmax; s += nb) {
     const int64_t b = (kmax - s) < nb ? (kmax - s) : nb;
     // 1. panel: columns s..s+b, rows s..m
-    if ((rc = pb_getrf_panel(m - s, b, A + s * lda + s, lda, ipiv + s, info, s, nullptr, st))) return launch_check(rc);
+    if ((rc = pb_getrf_panel(m - s, b, A + s * lda + s, lda, ipiv + s, info, s, work, st))) return launch_check(rc);
     // 2. the panel's swaps on the columns left and right of it
     if (s > 0 && (rc = pb_laswp(s, A, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);
     if (s + b < n && (rc = pb_laswp(n - s - b, A + s + b, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);

@@ -287,6 +287,7 @@ int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done[idx] = true;
   }
+  pb_count_launch();
   kern<<<grid, C::NTHR, smem, st>>>(P);
   return 0;
 }
@@ -317,6 +318,7 @@ int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream
   if (P.m == 0 || P.n == 0) return 0;
   const dim3 grid((unsigned)((P.n + 127) / 128), (unsigned)P.m);
   if (P.m > 65535) return PB_ERR_TOO_LARGE;
+  pb_count_launch();
   pg::k_gemm_naive<<<grid, 128, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
   return 0;
 }

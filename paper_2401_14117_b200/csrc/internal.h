@@ -13,7 +13,8 @@ int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream
 
 // lapack.cu
 int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
-                   int64_t row_base, const int32_t* stop_flag, cudaStream_t st);
+                   int64_t row_base, void* ws, cudaStream_t st);
+size_t pb_panel_ws_bytes();
 int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
              int64_t ipiv_base, cudaStream_t st);
 int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st);
@@ -24,3 +25,6 @@ int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64
 int pb_from_f64(const double* x, uint32_t* out, int64_t count, cudaStream_t st);
 int pb_to_f64(const uint32_t* p, double* out, int64_t count, cudaStream_t st);
 int pb_gemm_guarded(const pg::Params& P, bool transb, bool syrk, const int32_t* stop_flag, cudaStream_t st);
+
+// number of kernels this library has launched (posit_kernel_launches)
+void pb_count_launch();

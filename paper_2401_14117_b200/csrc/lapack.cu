@@ -4,11 +4,14 @@
 // the elementwise / conversion kernels.  All on the device, stream-ordered.
 //
 // Order contract (reading Q6): every element receives its updates
-// one product at a time in ascending k; the TRSMs are blocked into a small
-// in-block substitution plus a fast-path GEMM for the rows/columns beyond the
-// block, which is a traversal change only.
+// one product at a time in ascending k.  The panel and the diagonal-block
+// Cholesky are recursive (LAPACK getrf2 / potrf2 traversal) and the TRSMs are
+// blocked into a 32-wide in-block substitution plus a fast-path GEMM for the
+// rows/columns beyond the block -- traversal changes only, so the bits equal
+// the textbook loops.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "gemm.cuh"
 #include "internal.h"
 
@@ -19,7 +22,7 @@ using p32::div;
 using p32::mul;
 using p32::sub;
 
-constexpr int PIV_THREADS = 1024;
+constexpr int TB = 32;                 // in-block TRSM / potf2 leaf width (one warp)
 
 // abs of a pattern compared as a signed int: NaR stays INT32_MIN (the minimum)
 __device__ __forceinline__ int32_t abs_key(uint32_t a) {
@@ -27,63 +30,110 @@ __device__ __forceinline__ int32_t abs_key(uint32_t a) {
   return s < 0 ? (int32_t)(0u - a) : s;
 }
 
-// Column j of the m x b panel: pivot search over rows j..m-1 (max abs, ties ->
-// smallest row, reading Q10), ipiv, swap inside the panel, divide (Q8, Q11).
-__global__ void __launch_bounds__(PIV_THREADS) k_panel_pivot(uint32_t* A, int64_t lda, int64_t m, int64_t b, int64_t j,
-                                                             int32_t* ipiv, int32_t* info, int64_t row_base) {
-  __shared__ unsigned long long red[PIV_THREADS / 32];
-  __shared__ int64_t s_p;
-  __shared__ uint32_t s_v;
-  unsigned long long best = 0ull;
-  for (int64_t r = j + threadIdx.x; r < m; r += blockDim.x) {
-    const uint32_t key = (uint32_t)abs_key(A[r * lda + j]) ^ 0x80000000u;   // signed -> unsigned order
-    const unsigned long long k64 = ((unsigned long long)key << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)r);
-    best = k64 > best ? k64 : best;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-    best = other > best ? other : best;
-  }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-      best = other > best ? other : best;
-    }
-    if (threadIdx.x == 0) {
-      const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
-      s_p = p;
-      s_v = A[p * lda + j];
-      ipiv[j] = (int32_t)(row_base + p + 1);
-      if (s_v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
-    }
-  }
-  __syncthreads();
-  const int64_t p = s_p;
-  const uint32_t v = s_v;
-  if (v == 0u) return;                      // zero pivot: no swap, no division (Q11)
-  if (p != j) {
-    for (int64_t c = threadIdx.x; c < b; c += blockDim.x) {
-      const uint32_t t = A[j * lda + c];
-      A[j * lda + c] = A[p * lda + c];
-      A[p * lda + c] = t;
-    }
-    __syncthreads();
-  }
-  for (int64_t r = j + 1 + threadIdx.x; r < m; r += blockDim.x) A[r * lda + j] = div(A[r * lda + j], v);
+// 64-bit pivot key: larger abs first, then the smaller row (reading Q10)
+__device__ __forceinline__ unsigned long long piv_key(uint32_t a, int64_t r) {
+  const uint32_t k = (uint32_t)abs_key(a) ^ 0x80000000u;                 // signed -> unsigned order
+  return ((unsigned long long)k << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)r);
 }
 
-// a_rq <- a_rq (-) a_rj (x) a_jq for j < r < m, j < q < b  (one thread per element)
-__global__ void k_panel_update(uint32_t* A, int64_t lda, int64_t m, int64_t b, int64_t j) {
-  const int64_t w = b - j - 1;
+__device__ __forceinline__ unsigned long long block_max(unsigned long long v, unsigned long long* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      v = w > v ? w : v;
+    }
+  }
+  return v;   // valid in thread 0
+}
+
+// ---- LU leaf (column by column, multi-CTA) ----------------------------------
+// Workspace: key[0..w) (uint64, zeroed per leaf) and a CTA counter.
+struct LeafWs {
+  unsigned long long key[64];
+  unsigned int done;
+};
+
+// key[0] <- max over rows 0..m-1 of column 0
+__global__ void k_leaf_colmax(const uint32_t* A, int64_t lda, int64_t m, LeafWs* ws) {
+  __shared__ unsigned long long red[32];
+  unsigned long long best = 0ull;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = piv_key(A[r * lda], r);
+    best = k > best ? k : best;
+  }
+  best = block_max(best, red);
+  if (threadIdx.x == 0) atomicMax(&ws->key[0], best);
+}
+
+// Column j: p = the key's row; ipiv, info; swap rows j and p on the leaf's
+// other columns (CTA 0); divide rows j+1..m-1 of column j by the pivot v.  The
+// two words of column j that move (A[j][j], A[p][j]) are written by the CTA
+// that finishes last, after every CTA has read v (threadfence counter).
+__global__ void k_leaf_swap_div(uint32_t* A, int64_t lda, int64_t m, int64_t w, int64_t j, LeafWs* ws,
+                                int32_t* ipiv, int32_t* info, int64_t row_base) {
+  __shared__ bool last;
+  const unsigned long long key = ws->key[j];
+  const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+  const uint32_t v = A[p * lda + j];
+  const uint32_t ajj = A[j * lda + j];
+  if (v == 0u) {                                          // zero pivot: no swap, no division (Q11)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ipiv[j] = (int32_t)(row_base + p + 1);
+      if (*info == 0) *info = (int32_t)(row_base + j + 1);
+    }
+    return;
+  }
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) ipiv[j] = (int32_t)(row_base + p + 1);
+    if (p != j) {
+      for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+        if (c == j) continue;
+        const uint32_t t = A[j * lda + c];
+        A[j * lda + c] = A[p * lda + c];
+        A[p * lda + c] = t;
+      }
+    }
+  }
+  for (int64_t r = j + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
+    if (r != p) A[r * lda + j] = div(A[r * lda + j], v);
+  // last CTA: the moved words of column j
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    ws->done = 0u;
+    if (p != j) {
+      A[j * lda + j] = v;
+      A[p * lda + j] = div(ajj, v);
+    }
+  }
+}
+
+// a_rq <- a_rq (-) a_rj (x) a_jq for j < r < m, j < q < w; the new column j+1
+// feeds key[j+1] (rows j+1..m-1).
+__global__ void k_leaf_update(uint32_t* A, int64_t lda, int64_t m, int64_t w, int64_t j, LeafWs* ws) {
+  __shared__ unsigned long long red[32];
+  const int64_t wq = w - j - 1;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (m - j - 1) * w) return;
-  const int64_t r = j + 1 + e / w, q = j + 1 + e % w;
-  A[r * lda + q] = sub(A[r * lda + q], mul(A[r * lda + j], A[j * lda + q]));
+  unsigned long long best = 0ull;
+  if (e < (m - j - 1) * wq) {
+    const int64_t r = j + 1 + e / wq, q = j + 1 + e % wq;
+    const uint32_t nv = sub(A[r * lda + q], mul(A[r * lda + j], A[j * lda + q]));
+    A[r * lda + q] = nv;
+    if (q == j + 1) best = piv_key(nv, r);
+  }
+  best = block_max(best, red);
+  if (threadIdx.x == 0 && best != 0ull) atomicMax(&ws->key[j + 1], best);
 }
 
 // rows k1..k2-1 swapped with ipiv[k]-1-base, in order, for columns [0, ncols)
@@ -101,62 +151,88 @@ __global__ void k_laswp(uint32_t* A, int64_t lda, int64_t ncols, int64_t k1, int
   }
 }
 
-// In-block forward substitution, unit lower: rows i0..i0+ib-1 of B, one thread per column.
-__global__ void k_trsm_llnu_block(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, int64_t i0, int64_t ib,
-                                  int64_t n) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  for (int64_t i = i0; i < i0 + ib; i++) {
-    uint32_t v = B[i * ldb + c];
-    for (int64_t k = i0; k < i; k++) v = sub(v, mul(L[i * ldl + k], B[k * ldb + c]));
-    B[i * ldb + c] = v;
+// ---- TRSM in-block kernels (32-wide, right-looking across a warp) -----------
+// Unit lower, left: rows i0..i0+ib-1 of B (ib <= 32).  CTA = 32 warps = 32
+// columns; the 32 x 32 tile goes through shared memory (coalesced); warp w
+// owns column w with lane = row: step k broadcasts the final b_k by shuffle
+// and rows i > k apply b_i <- b_i (-) l_ik (x) b_k (ascending k per element).
+__global__ void __launch_bounds__(1024) k_trsm_llnu_blk(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t i0, int64_t ib, int64_t n) {
+  __shared__ uint32_t sb[TB][TB + 1];
+  __shared__ uint32_t sl[TB][TB + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * TB;
+  if (wid < ib) {
+    sl[wid][lane] = lane < wid ? L[(i0 + wid) * ldl + i0 + lane] : 0u;
+    sb[wid][lane] = (c0 + lane < n) ? B[(i0 + wid) * ldb + c0 + lane] : 0u;
   }
+  __syncthreads();
+  uint32_t b = lane < ib ? sb[lane][wid] : 0u;
+  for (int k = 0; k < ib - 1; k++) {
+    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, b, k);
+    if (lane > k && lane < ib) b = sub(b, mul(sl[lane][k], bk));
+  }
+  if (lane < ib) sb[lane][wid] = b;
+  __syncthreads();
+  if (wid < ib && c0 + lane < n) B[(i0 + wid) * ldb + c0 + lane] = sb[wid][lane];
 }
 
-// In-block right solve with L^T, non-unit: columns j0..j0+jb-1 of B, one thread per row.
-__global__ void k_trsm_rltn_block(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, int64_t j0, int64_t jb,
-                                  int64_t m, const int32_t* stop) {
+// Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 32).
+// Warp per row of B, lane = column (coalesced): step k finalises b_k <- b_k (/)
+// l_kk, broadcasts it, and columns j > k apply b_j <- b_j (-) b_k (x) l_jk.
+__global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t j0, int64_t jb, int64_t m, const int32_t* stop) {
+  __shared__ uint32_t sl[TB][TB + 1];
   if (stop != nullptr && *stop != 0) return;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid < jb) sl[wid][lane] = lane <= wid ? L[(j0 + wid) * ldl + j0 + lane] : 0u;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * 32 + wid;
   if (r >= m) return;
-  for (int64_t j = j0; j < j0 + jb; j++) {
-    uint32_t v = B[r * ldb + j];
-    for (int64_t k = j0; k < j; k++) v = sub(v, mul(B[r * ldb + k], L[j * ldl + k]));
-    B[r * ldb + j] = div(v, L[j * ldl + j]);
+  uint32_t b = lane < jb ? B[r * ldb + j0 + lane] : 0u;
+  for (int k = 0; k < jb; k++) {
+    if (lane == k) b = div(b, sl[k][k]);
+    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, b, k);
+    if (lane > k && lane < jb) b = sub(b, mul(bk, sl[lane][k]));
   }
+  if (lane < jb) B[r * ldb + j0 + lane] = b;
 }
 
-// Unblocked Cholesky of the b x b diagonal block (lower), one CTA (reading Q9).
-__global__ void __launch_bounds__(1024) k_potf2(uint32_t* A, int64_t lda, int64_t b, int32_t* info, int64_t row_base) {
-  __shared__ int s_fail;
-  __shared__ uint32_t s_d;
-  if (*info != 0) return;                       // an earlier block failed: stop
-  for (int64_t k = 0; k < b; k++) {
+// ---- Cholesky leaf: b <= 32 diagonal block in shared memory, one CTA ---------
+// Textbook loop (reading Q9): for k: if signed(a_kk) <= 0 -> info = k+1, stop;
+// a_kk <- sqrt(a_kk); a_ik <- a_ik (/) a_kk; a_ij <- a_ij (-) a_ik (x) a_jk.
+__global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, int64_t b, int32_t* info,
+                                                     int64_t row_base) {
+  __shared__ uint32_t s[TB][TB + 1];
+  __shared__ int fail;
+  if (*info != 0) return;                                  // an earlier block failed: stop
+  const int i = threadIdx.x >> 5, j = threadIdx.x & 31;    // row, column
+  const bool in = i < b && j <= i;
+  if (in) s[i][j] = A[i * lda + j];
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  int k = 0;
+  for (; k < b; k++) {
     if (threadIdx.x == 0) {
-      const uint32_t v = A[k * lda + k];
-      if ((int32_t)v <= 0) {                     // zero, negative or NaR pivot
-        s_fail = 1;
+      const uint32_t v = s[k][k];
+      if ((int32_t)v <= 0) {                               // zero, negative or NaR pivot
+        fail = 1;
         *info = (int32_t)(row_base + k + 1);
       } else {
-        s_fail = 0;
-        s_d = p32::sqrt(v);
-        A[k * lda + k] = s_d;
+        s[k][k] = p32::sqrt(v);
       }
     }
     __syncthreads();
-    if (s_fail) return;
-    const uint32_t d = s_d;
-    for (int64_t i = k + 1 + threadIdx.x; i < b; i += blockDim.x) A[i * lda + k] = div(A[i * lda + k], d);
+    if (fail) break;
+    if (j == k && i > k && i < b) s[i][k] = div(s[i][k], s[k][k]);
     __syncthreads();
-    const int64_t w = b - k - 1;
-    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
-      const int64_t i = k + 1 + e / w, jj = k + 1 + e % w;
-      if (jj <= i) A[i * lda + jj] = sub(A[i * lda + jj], mul(A[i * lda + k], A[jj * lda + k]));
-    }
+    if (in && j > k) s[i][j] = sub(s[i][j], mul(s[i][k], s[j][k]));
     __syncthreads();
   }
+  if (in) A[i * lda + j] = s[i][j];
 }
 
+// ---- elementwise / conversion ------------------------------------------------
 __global__ void k_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t x = a[i];
@@ -188,6 +264,12 @@ inline unsigned grid_for(int64_t count, int threads) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+inline unsigned rows_grid(int64_t rows, int threads) {
+  int64_t g = (rows + threads - 1) / threads;
+  if (g > 148 * 4) g = 148 * 4;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
 }  // namespace pl
 
 using namespace pl;
@@ -196,14 +278,61 @@ static int last_launch() {
   return cudaPeekAtLastError() == cudaSuccess ? 0 : POSIT_ECUDA;
 }
 
-int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
-                   const int32_t* stop, cudaStream_t st) {
-  (void)stop;
-  const int64_t jmax = m < b ? m : b;
+size_t pb_panel_ws_bytes() { return sizeof(LeafWs); }
+
+static int64_t panel_leaf() {
+  static int64_t leaf = -1;
+  if (leaf < 0) {
+    const char* e = getenv("POSIT_PANEL_LEAF");
+    leaf = e ? atoll(e) : 32;
+    if (leaf < 1) leaf = 1;
+    if (leaf > 64) leaf = 64;
+  }
+  return leaf;
+}
+
+// Unblocked leaf (w <= 64 columns): per column one swap/divide launch and one
+// update launch that also searches the next column's pivot.
+static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
+                      LeafWs* ws, cudaStream_t st) {
+  if (cudaMemsetAsync(ws, 0, sizeof(LeafWs), st) != cudaSuccess) return POSIT_ECUDA;
+  pb_count_launch();
+  k_leaf_colmax<<<rows_grid(m, 256), 256, 0, st>>>(A, lda, m, ws);
+  const int64_t jmax = m < w ? m : w;
   for (int64_t j = 0; j < jmax; j++) {
-    k_panel_pivot<<<1, PIV_THREADS, 0, st>>>(A, lda, m, b, j, ipiv, info, row_base);
-    const int64_t cnt = (m - j - 1) * (b - j - 1);
-    if (cnt > 0) k_panel_update<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(A, lda, m, b, j);
+    pb_count_launch();
+    k_leaf_swap_div<<<rows_grid(m - j - 1, 256), 256, 0, st>>>(A, lda, m, w, j, ws, ipiv, info, row_base);
+    const int64_t cnt = (m - j - 1) * (w - j - 1);
+    if (cnt > 0) {
+      pb_count_launch();
+      k_leaf_update<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(A, lda, m, w, j, ws);
+    }
+  }
+  return last_launch();
+}
+
+// Recursive panel LU (the traversal of LAPACK getrf2): factor the left half,
+// apply its swaps to the right half, U12 by TRSM, the right half's update by
+// the fast GEMM, factor the right half, apply its swaps to the left half.
+// Every element still receives its products one at a time in ascending k
+// (reading Q6), so the bits equal the column-by-column loop.
+int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
+                   void* ws, cudaStream_t st) {
+  const int64_t w = m < b ? m : b;
+  const int64_t leaf = panel_leaf();
+  if (w <= leaf) return getrf_leaf(m, b, A, lda, ipiv, info, row_base, static_cast<LeafWs*>(ws), st);
+  int64_t w1 = ((w / 2 + leaf - 1) / leaf) * leaf;
+  if (w1 >= w) w1 = w - leaf;
+  int rc;
+  if ((rc = pb_getrf_panel(m, w1, A, lda, ipiv, info, row_base, ws, st))) return rc;
+  if ((rc = pb_laswp(b - w1, A + w1, lda, 0, w1, ipiv, row_base, st))) return rc;
+  if ((rc = pb_trsm_llnu(w1, b - w1, A, lda, A + w1, lda, st))) return rc;
+  if (m > w1) {
+    pg::Params P{m - w1, b - w1, w1, A + w1 * lda, lda, A + w1, lda, A + w1 * lda + w1, lda, 1, 1, nullptr};
+    if ((rc = pb_launch_gemm(P, false, false, st))) return rc;
+    if ((rc = pb_getrf_panel(m - w1, b - w1, A + w1 * lda + w1, lda, ipiv + w1, info, row_base + w1, ws, st)))
+      return rc;
+    if ((rc = pb_laswp(w1, A + w1 * lda, lda, 0, w - w1, ipiv + w1, row_base + w1, st))) return rc;
   }
   return last_launch();
 }
@@ -211,17 +340,19 @@ int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv
 int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv, int64_t ipiv_base,
              cudaStream_t st) {
   if (ncols <= 0 || k2 <= k1) return 0;
+  pb_count_launch();
   k_laswp<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(A, lda, ncols, k1, k2, ipiv, ipiv_base);
   return last_launch();
 }
 
-static constexpr int64_t TRSM_BLK = 16;
-
 int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
-  for (int64_t i0 = 0; i0 < m; i0 += TRSM_BLK) {
-    const int64_t ib = (m - i0) < TRSM_BLK ? (m - i0) : TRSM_BLK;
-    k_trsm_llnu_block<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+  for (int64_t i0 = 0; i0 < m; i0 += TB) {
+    const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
+    if (ib > 1) {
+      pb_count_launch();
+      k_trsm_llnu_blk<<<(unsigned)((n + TB - 1) / TB), 1024, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+    }
     if (i0 + ib < m) {
       pg::Params P{m - i0 - ib, n, ib, L + (i0 + ib) * ldl + i0, ldl, B + i0 * ldb, ldb, B + (i0 + ib) * ldb, ldb,
                    1, 1, nullptr};
@@ -235,9 +366,10 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
 int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, const int32_t* stop,
                  cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
-  for (int64_t j0 = 0; j0 < n; j0 += TRSM_BLK) {
-    const int64_t jb = (n - j0) < TRSM_BLK ? (n - j0) : TRSM_BLK;
-    k_trsm_rltn_block<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(L, ldl, B, ldb, j0, jb, m, stop);
+  for (int64_t j0 = 0; j0 < n; j0 += TB) {
+    const int64_t jb = (n - j0) < TB ? (n - j0) : TB;
+    pb_count_launch();
+    k_trsm_rltn_blk<<<(unsigned)((m + 31) / 32), 1024, 0, st>>>(L, ldl, B, ldb, j0, jb, m, stop);
     if (j0 + jb < n) {
       // B[:, j0+jb:] -= B[:, j0:j0+jb] * L[j0+jb:, j0:j0+jb]^T   (NT GEMM, K = jb)
       pg::Params P{m, n - j0 - jb, jb, B + j0, ldb, L + (j0 + jb) * ldl + j0, ldl, B + j0 + jb, ldb, 1, 1, stop};
@@ -248,25 +380,43 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   return last_launch();
 }
 
+// Recursive diagonal-block Cholesky (the traversal of LAPACK potrf2): leaf
+// blocks of <= 32 in shared memory, TRSM + SYRK between them.  Every stage
+// is a no-op once *info != 0.
 int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_base, cudaStream_t st) {
-  k_potf2<<<1, 1024, 0, st>>>(A, lda, b, info, row_base);
-  return last_launch();
+  if (b <= 0) return 0;
+  if (b <= TB) {
+    pb_count_launch();
+    k_potf2_leaf<<<1, 1024, 0, st>>>(A, lda, b, info, row_base);
+    return last_launch();
+  }
+  int64_t b1 = ((b / 2 + TB - 1) / TB) * TB;
+  if (b1 >= b) b1 = b - TB;
+  int rc;
+  if ((rc = pb_potf2(b1, A, lda, info, row_base, st))) return rc;
+  if ((rc = pb_trsm_rltn(b - b1, b1, A, lda, A + b1 * lda, lda, info, st))) return rc;
+  pg::Params P{b - b1, b - b1, b1, A + b1 * lda, lda, A + b1 * lda, lda, A + b1 * lda + b1, lda, 1, 1, info};
+  if ((rc = pb_launch_gemm(P, true, true, st))) return rc;
+  return pb_potf2(b - b1, A + b1 * lda + b1, lda, info, row_base + b1, st);
 }
 
 int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, cudaStream_t st) {
   if (count <= 0) return 0;
+  pb_count_launch();
   k_vec_op<<<grid_for(count, 256), 256, 0, st>>>(op, a, b, out, count);
   return last_launch();
 }
 
 int pb_from_f64(const double* x, uint32_t* out, int64_t count, cudaStream_t st) {
   if (count <= 0) return 0;
+  pb_count_launch();
   k_from_f64<<<grid_for(count, 256), 256, 0, st>>>(x, out, count);
   return last_launch();
 }
 
 int pb_to_f64(const uint32_t* p, double* out, int64_t count, cudaStream_t st) {
   if (count <= 0) return 0;
+  pb_count_launch();
   k_to_f64<<<grid_for(count, 256), 256, 0, st>>>(p, out, count);
   return last_launch();
 }

@@ -125,7 +125,17 @@ def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, i
     ipiv (int32, n) receives the global 1-based pivots on EVERY rank; info
     (int32, 1) the first zero-pivot column (1-based) or 0, on every rank.
     """
-    ops = CudaOps() if ops is None else ops
+    steps = getrf_dist_steps(A_local, desc, ipiv, info, CudaOps() if ops is None else ops)
+    for s, buf in enumerate(steps):
+        if desc.nprocs > 1:
+            dist.broadcast(buf, src=desc.owner(s), group=group)
+
+
+def getrf_dist_steps(A_local, desc: BlockCyclic1D, ipiv, info, ops):
+    """The per-rank schedule of getrf_dist as a generator: for each panel step
+    s it runs the panel phase, yields the packed [panel | ipiv | info] buffer
+    (filled on the owner), expects it to hold the owner's data when resumed
+    (the broadcast), and then runs the swap / TRSM / trailing-GEMM phase."""
     n, nb, P, me = desc.n, desc.nb, desc.nprocs, desc.rank
     if A_local.shape != (n, desc.local_cols()):
         raise ValueError(f"A_local has shape {tuple(A_local.shape)}, expected {(n, desc.local_cols())}")
@@ -147,8 +157,7 @@ def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, i
             panel.copy_(Ap)
             buf[m * b: m * b + b].copy_(ipiv[r0: r0 + b])
             buf[m * b + b: m * b + b + 1].copy_(my_info)
-        if P > 1:
-            dist.broadcast(buf, src=o, group=group)
+        yield buf
         if me != o:
             ipiv[r0: r0 + b].copy_(buf[m * b: m * b + b])
         # first zero pivot so far, identical on every rank (the owner's counter is cumulative)

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", PB.LIB_PATH], capture_output=True, text=True).stdout
     for n in names:
         assert re.search(rf"\bT {n}\b", out), n
-    assert L.posit_abi_version() == 1
+    assert L.posit_abi_version() == 2
 
 
 def test_library_is_sm100a():
