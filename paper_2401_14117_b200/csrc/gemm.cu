@@ -19,9 +19,9 @@ struct Cfg {
   static constexpr int AQ = (AQN + NTHR - 1) / NTHR;            // A quads per thread (last may idle)
   static constexpr int BQ = (BQN + NTHR - 1) / NTHR;
   struct Smem {
-    uint2 a[2][BK][BM];
-    uint2 b[2][BK][BN];
-    uint2 tp[TSIZE];
+    uint4 a[2][BK][BM];
+    uint4 b[2][BK][BN];
+    uint4 tp[TSIZE];
     uint4 tx[TSIZE];
   };
 };
@@ -37,7 +37,7 @@ __device__ __forceinline__ uint32_t mac_generic(uint32_t c, uint32_t a, uint32_t
 // arguments: keeps the fast loop's accumulators in registers).  Returns the
 // new accumulator (x = M, y = E, z = s) and w = 1 if the result cannot live
 // in the fast accumulator.
-__device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, uint32_t sg, const uint32_t* A, int64_t lda,
+__device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, int32_t sg, const uint32_t* A, int64_t lda,
                                         const uint32_t* B, int64_t ldb, int neg, int64_t r, int64_t cc, int64_t k0,
                                         int kmax, int transb) {
   Acc acc{M, E, sg};
@@ -49,7 +49,7 @@ __device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, uint32_t sg, cons
     c = mac_generic(c, a, b, neg);
   }
   const uint32_t bad = acc_decode(c, acc) ? 0u : 1u;
-  return make_uint4(acc.M, (uint32_t)acc.E, acc.s, bad);
+  return make_uint4(acc.M, (uint32_t)acc.E, (uint32_t)acc.sg, bad);
 }
 
 // Whole chain of one output with the generic path (the recompute of a thread
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   const uint32_t flip = P.neg ? 1u : 0u;
   fill_tables(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
   MacConst K;
-  K.one = (uint32_t)P.one; K.two = 2u * K.one; K.eight = 8u * K.one; K.sixteen = 16u * K.one;
+  K.one = (uint32_t)P.one; K.sixteen = 16u * K.one;
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + TBIAS);
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + TBIAS) - 30u * 16u;   // indexed by Ex + 30
 
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (kmax == BK) {
 #pragma unroll 2
         for (int kk = 0; kk < BK; kk++) {
-          uint2 av[TM], bv[TN];
+          uint4 av[TM], bv[TN];
 #pragma unroll
           for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
 #pragma unroll
@@ -189,11 +189,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, K, badacc);
+            for (int j = 0; j < TN; j++)
+              mac(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y, (int32_t)bv[j].z,
+                  K, badacc);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
-          uint2 av[TM], bv[TN];
+          uint4 av[TM], bv[TN];
 #pragma unroll
           for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
 #pragma unroll
@@ -201,7 +203,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) mac(acc[i][j], av[i].x, av[i].y, bv[j].x, bv[j].y, K, badacc);
+            for (int j = 0; j < TN; j++)
+              mac(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y, (int32_t)bv[j].z,
+                  K, badacc);
         }
       }
       // once per k-slab: fold the accumulated flags, bound the scales (table range)
@@ -219,9 +223,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         for (int j = 0; j < TN; j++) {
           const int64_t r = row0 + ty * TM + i, cc = col0 + tx * TN + j;
           if (r < P.m && cc < P.n) {
-            const uint4 o = slow_slab(acc[i][j].M, acc[i][j].E, acc[i][j].s, P.A, P.lda, P.B, P.ldb, P.neg, r, cc,
+            const uint4 o = slow_slab(acc[i][j].M, acc[i][j].E, acc[i][j].sg, P.A, P.lda, P.B, P.ldb, P.neg, r, cc,
                                       k0, kmax, TRANS_B ? 1 : 0);
-            acc[i][j].M = o.x; acc[i][j].E = (int32_t)o.y; acc[i][j].s = o.z; bad = bad | (o.w != 0u);
+            acc[i][j].M = o.x; acc[i][j].E = (int32_t)o.y; acc[i][j].sg = (int32_t)o.z; bad = bad | (o.w != 0u);
           }
         }
       }
@@ -296,7 +300,7 @@ int variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("POSIT_GEMM_VARIANT");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 2;
   }
   return v;
 }

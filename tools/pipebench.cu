@@ -33,6 +33,17 @@ __global__ void kern(unsigned* out, unsigned seed, long long* cyc) {
       if (OP == 12) asm volatile("shr.u32 %0, %0, 3; add.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(b));
       if (OP == 13) asm volatile("min.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(b));
       if (OP == 14) asm volatile("abs.s32 %0, %0;" : "+r"(r[i]));
+      if (OP == 15) { unsigned lo, hi; asm volatile("mul.wide.u32 %0, %2, %3;" : "=l"(*(unsigned long long*)&lo) : "r"(0), "r"(r[i]), "r"(b)); }
+      if (OP == 16) asm volatile("{.reg .u64 w; mul.wide.u32 w, %0, %1; cvt.u32.u64 %0, w;}" : "+r"(r[i]) : "r"(b));
+      if (OP == 17) asm volatile("{.reg .u64 w; .reg .u32 l, h; mul.wide.u32 w, %0, %1; mov.b64 {l, h}, w; xor.b32 %0, l, h;}" : "+r"(r[i]) : "r"(b));
+      if (OP == 18) asm volatile("mad.hi.u32 %0, %0, %1, %0;" : "+r"(r[i]) : "r"(b));
+      if (OP == 19) asm volatile("shf.r.clamp.b32 %0, %0, %1, %0;" : "+r"(r[i]) : "r"(c));
+      if (OP == 20) asm volatile("{.reg .f32 f; cvt.rn.f32.u32 f, %0; mov.b32 %0, f;}" : "+r"(r[i]));
+      if (OP == 21) asm volatile("{.reg .u32 t; add.cc.u32 t, %0, %1; addc.u32 %0, %0, %2;}" : "+r"(r[i]) : "r"(b), "r"(c));
+      if (OP == 22) asm volatile("{.reg .f64 d; mov.b64 d, {%0, %1}; fma.rn.f64 d, d, d, d; mov.b64 {%0, %1}, d;}" : "+r"(r[i]) : "r"(b));
+      if (OP == 23) asm volatile("popc.b32 %0, %0;" : "+r"(r[i]));
+      if (OP == 24) asm volatile("add.u32 %0, %0, 77;" : "+r"(r[i]));
+      if (OP == 25) asm volatile("{.reg .u32 t; .reg .pred p; setp.ne.u32 p, %0, 0; selp.u32 t, 1, 0, p; or.b32 %0, %0, t;}" : "+r"(r[i]));
     }
   }
   long long t1 = clock64();
@@ -73,7 +84,17 @@ int main() {
   run<11>("add+add 3-operand", 2, out, cyc, nsm, false);
   run<12>("shr+add (LEA.HI)", 2, out, cyc, nsm, false);
   run<13>("min.u32 (IMNMX)", 1, out, cyc, nsm, false);
-  run<14>("abs (IABS)", 1, out, cyc, nsm, true);
+  run<14>("abs (IABS)", 1, out, cyc, nsm, false);
+  run<16>("mul.wide.u32 lo (IMAD.WIDE?)", 1, out, cyc, nsm, false);
+  run<17>("mul.wide.u32 + xor (IMAD.WIDE + LOP3)", 2, out, cyc, nsm, false);
+  run<18>("mad.hi.u32 with addend", 1, out, cyc, nsm, false);
+  run<19>("shf.r.clamp funnel", 1, out, cyc, nsm, false);
+  run<20>("cvt.rn.f32.u32 (I2F)", 1, out, cyc, nsm, false);
+  run<21>("add.cc + addc pair", 2, out, cyc, nsm, false);
+  run<22>("fma.rn.f64 (DFMA)", 1, out, cyc, nsm, false);
+  run<23>("popc (POPC)", 1, out, cyc, nsm, false);
+  run<24>("add.u32 imm (VIADD?)", 1, out, cyc, nsm, false);
+  run<25>("setp+selp+or", 3, out, cyc, nsm, true);
   printf("}\n");
   return 0;
 }

@@ -2,7 +2,7 @@
 
     python tools/sass_stats.py [kernel-substring]
 Counts the instructions of every backward-branch loop that contains IMAD.HI
-(one per posit product) in libposit_b200.so, to estimate issue slots per MAC
+(FLO: one per posit MAC) in libposit_b200.so, to estimate issue slots per MAC
 before spending GPU time.
 """
 import collections
@@ -31,7 +31,7 @@ def main():
             if m and int(m.group(1), 16) < a:
                 tgt = int(m.group(1), 16)
                 body = [x[1] for x in ins if tgt <= x[0] <= a]
-                nhi = sum(1 for x in body if "IMAD.HI" in x)
+                nhi = sum(1 for x in body if x.startswith("FLO"))
                 if nhi == 0:
                     continue
                 print(f"  loop [{tgt:#x},{a:#x}] len {len(body)} products {nhi} -> {len(body) / nhi:.2f} instr/MAC")
