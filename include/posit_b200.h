@@ -170,6 +170,22 @@ size_t posit_potrf_work_bytes(int64_t n, int64_t nb);
 int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, int64_t nb, void* work,
                 size_t work_bytes, void* stream);
 
+/*
+ * posit_getrs / posit_potrs -- one right-hand side b (length n, DEVICE,
+ * overwritten by x) solved with the factors of posit_getrf / posit_potrf:
+ * the Rgetrs / Rpotrs of the paper's accuracy study.
+ * getrs: b <- P b, L y = b (unit lower), U x = y.  potrs: L y = b, L^T x = y.
+ * Order (reading Q21, reference-BLAS trsv): forward substitution gives each
+ * element its updates in ascending k, back substitution in descending k;
+ * every multiply, subtract and divide is one correctly rounded posit op.
+ * trans must be 'N' / uplo 'L' (else POSIT_ENOTSUP); n <= 51200 (shared
+ * memory, else POSIT_ENOTSUP).  Latency-bound single-CTA kernels: a report
+ * tool, not the hot path.
+ */
+int posit_getrs(char trans, int64_t n, const uint32_t* LU, int64_t lda, const int32_t* ipiv, uint32_t* b,
+                void* stream);
+int posit_potrs(char uplo, int64_t n, const uint32_t* L, int64_t lda, uint32_t* b, void* stream);
+
 /* Conversions: binary64 -> posit rounds once (RNE), NaN/Inf -> NaR,
  * -0 -> 0, subnormals -> +-minpos; posit -> binary64 is exact (NaR -> NaN). */
 int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream);

@@ -468,8 +468,13 @@ int or_potrf_lower(int64_t n, uint32_t* A, int64_t lda, int32_t* info) {
     return 0;
 }
 
-/* Solves for the accuracy report (Rgetrs / Rpotrs), one RHS,
- * in Posit(32,2), ascending-k substitution. */
+/* Solves for the accuracy report (Rgetrs / Rpotrs), one RHS, in
+ * Posit(32,2), in the loop order of the reference BLAS trsv that MPLAPACK's
+ * Rtrsv follows (reading Q21): forward substitution receives its
+ * updates in ascending k, back substitution in DESCENDING k (column-oriented
+ * "x_j final, then update every x_i, i < j" for U x = y; the dot-product
+ * form for L^T x = y, which runs i = n-1 .. j+1).  Written as the plain
+ * per-element loops. */
 int or_getrs(int64_t n, const uint32_t* LU, int64_t lda, const int32_t* ipiv, uint32_t* b) {
     for (int64_t k = 0; k < n; k++) {             /* apply P */
         const int64_t p = ipiv[k] - 1;
@@ -478,7 +483,7 @@ int or_getrs(int64_t n, const uint32_t* LU, int64_t lda, const int32_t* ipiv, ui
     for (int64_t i = 0; i < n; i++)               /* L y = Pb, unit lower */
         for (int64_t k = 0; k < i; k++) b[i] = psub(b[i], pmul(LU[i * lda + k], b[k]));
     for (int64_t i = n - 1; i >= 0; i--) {        /* U x = y */
-        for (int64_t k = i + 1; k < n; k++) b[i] = psub(b[i], pmul(LU[i * lda + k], b[k]));
+        for (int64_t k = n - 1; k > i; k--) b[i] = psub(b[i], pmul(LU[i * lda + k], b[k]));
         b[i] = pdiv(b[i], LU[i * lda + i]);
     }
     return 0;
@@ -490,7 +495,7 @@ int or_potrs_lower(int64_t n, const uint32_t* L, int64_t lda, uint32_t* b) {
         b[i] = pdiv(b[i], L[i * lda + i]);
     }
     for (int64_t i = n - 1; i >= 0; i--) {        /* L^T x = y */
-        for (int64_t k = i + 1; k < n; k++) b[i] = psub(b[i], pmul(L[k * lda + i], b[k]));
+        for (int64_t k = n - 1; k > i; k--) b[i] = psub(b[i], pmul(L[k * lda + i], b[k]));
         b[i] = pdiv(b[i], L[i * lda + i]);
     }
     return 0;

@@ -18,7 +18,7 @@ import os
 
 __all__ = [
     "lib", "PositError", "posit_gemm", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
-    "posit_getrf", "posit_getrf_panel", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
+    "posit_getrf", "posit_getrf_panel", "posit_getrs", "posit_potrs", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
     "posit_vec_op", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
 ]
 
@@ -60,6 +60,8 @@ def lib() -> ctypes.CDLL:
         L.posit_potrf.argtypes = [c_char, i64, vp, i64, vp, i64, vp, sz, vp]
         L.posit_potrf_work_bytes.argtypes = [i64, i64]
         L.posit_potrf_work_bytes.restype = sz
+        L.posit_getrs.argtypes = [c_char, i64, vp, i64, vp, vp, vp]
+        L.posit_potrs.argtypes = [c_char, i64, vp, i64, vp, vp]
         L.posit_from_f64.argtypes = [vp, vp, i64, vp]
         L.posit_to_f64.argtypes = [vp, vp, i64, vp]
         L.posit_vec_op.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp]
@@ -178,6 +180,18 @@ def posit_laswp(A, k1: int, k2: int, ipiv, ipiv_base: int = 0, stream=None) -> N
 def posit_potrf(A, info, nb: int = 256, stream=None) -> None:
     n = A.shape[0]
     _check(lib().posit_potrf(b"L", n, _ptr(A), _ld(A), _ptr(info), nb, None, 0, _stream(stream)), "posit_potrf")
+
+
+def posit_getrs(LU, ipiv, b, stream=None) -> None:
+    """b <- A^{-1} b in place with the posit_getrf factors (one RHS, device tensors)."""
+    n = LU.shape[0]
+    _check(lib().posit_getrs(b"N", n, _ptr(LU), _ld(LU), _ptr(ipiv), _ptr(b), _stream(stream)), "posit_getrs")
+
+
+def posit_potrs(L, b, stream=None) -> None:
+    """b <- A^{-1} b in place with the posit_potrf lower factor (one RHS, device tensors)."""
+    n = L.shape[0]
+    _check(lib().posit_potrs(b"L", n, _ptr(L), _ld(L), _ptr(b), _stream(stream)), "posit_potrs")
 
 
 def posit_from_f64(x, out=None, stream=None):

@@ -247,6 +247,23 @@ int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, i
   return cuda_check(cudaPeekAtLastError());
 }
 
+int posit_getrs(char trans, int64_t n, const uint32_t* LU, int64_t lda, const int32_t* ipiv, uint32_t* b,
+                void* stream) {
+  if (trans != 'N') return trans == 'T' ? POSIT_ENOTSUP : -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  if (n > 0 && (LU == nullptr || ipiv == nullptr || b == nullptr)) return -3;
+  return launch_check(pb_solve(false, n, LU, lda, ipiv, b, S(stream)));
+}
+
+int posit_potrs(char uplo, int64_t n, const uint32_t* L, int64_t lda, uint32_t* b, void* stream) {
+  if (uplo != 'L') return uplo == 'U' ? POSIT_ENOTSUP : -1;
+  if (n < 0) return -2;
+  if (lda < (n > 1 ? n : 1)) return -4;
+  if (n > 0 && (L == nullptr || b == nullptr)) return -3;
+  return launch_check(pb_solve(true, n, L, lda, nullptr, b, S(stream)));
+}
+
 int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream) {
   if (count < 0) return -3;
   return launch_check(pb_from_f64(x, out, count, S(stream)));

@@ -232,6 +232,60 @@ __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, i
   if (in) A[i * lda + j] = s[i][j];
 }
 
+// ---- one-RHS solves for the accuracy report (Rgetrs / Rpotrs) -----
+// One CTA; the right-hand side lives in shared memory.  Reference-BLAS trsv
+// loop order (reading Q21): forward substitution in ascending k, back
+// substitution in descending k, each step "x_k final, then update the rest".
+constexpr int SOLVE_THREADS = 1024;
+
+__global__ void __launch_bounds__(SOLVE_THREADS) k_getrs(int64_t n, const uint32_t* LU, int64_t lda,
+                                                         const int32_t* ipiv, uint32_t* b) {
+  extern __shared__ uint32_t sx[];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sx[i] = b[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int64_t k = 0; k < n; k++) {                       // apply P
+      const int64_t p = (int64_t)ipiv[k] - 1;
+      if (p != k) { const uint32_t t = sx[k]; sx[k] = sx[p]; sx[p] = t; }
+    }
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < n; k++) {                         // L y = P b (unit lower)
+    const uint32_t yk = sx[k];
+    for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) sx[i] = sub(sx[i], mul(LU[i * lda + k], yk));
+    __syncthreads();
+  }
+  for (int64_t k = n - 1; k >= 0; k--) {                    // U x = y
+    if (threadIdx.x == 0) sx[k] = div(sx[k], LU[k * lda + k]);
+    __syncthreads();
+    const uint32_t xk = sx[k];
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) sx[i] = sub(sx[i], mul(LU[i * lda + k], xk));
+    __syncthreads();
+  }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) b[i] = sx[i];
+}
+
+__global__ void __launch_bounds__(SOLVE_THREADS) k_potrs(int64_t n, const uint32_t* L, int64_t lda, uint32_t* b) {
+  extern __shared__ uint32_t sx[];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sx[i] = b[i];
+  __syncthreads();
+  for (int64_t k = 0; k < n; k++) {                         // L y = b
+    if (threadIdx.x == 0) sx[k] = div(sx[k], L[k * lda + k]);
+    __syncthreads();
+    const uint32_t yk = sx[k];
+    for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) sx[i] = sub(sx[i], mul(L[i * lda + k], yk));
+    __syncthreads();
+  }
+  for (int64_t k = n - 1; k >= 0; k--) {                    // L^T x = y
+    if (threadIdx.x == 0) sx[k] = div(sx[k], L[k * lda + k]);
+    __syncthreads();
+    const uint32_t xk = sx[k];
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) sx[i] = sub(sx[i], mul(L[k * lda + i], xk));
+    __syncthreads();
+  }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) b[i] = sx[i];
+}
+
 // ---- elementwise / conversion ------------------------------------------------
 __global__ void k_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
@@ -398,6 +452,22 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
   pg::Params P{b - b1, b - b1, b1, A + b1 * lda, lda, A + b1 * lda, lda, A + b1 * lda + b1, lda, 1, 1, info};
   if ((rc = pb_launch_gemm(P, true, true, st))) return rc;
   return pb_potf2(b - b1, A + b1 * lda + b1, lda, info, row_base + b1, st);
+}
+
+int pb_solve(bool chol, int64_t n, const uint32_t* A, int64_t lda, const int32_t* ipiv, uint32_t* b, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const size_t smem = (size_t)n * sizeof(uint32_t);
+  if (smem > 200 * 1024) return POSIT_ENOTSUP;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_getrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_potrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  pb_count_launch();
+  if (chol) k_potrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, b);
+  else k_getrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, ipiv, b);
+  return last_launch();
 }
 
 int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, cudaStream_t st) {

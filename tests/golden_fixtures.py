@@ -64,6 +64,13 @@ def spec_linalg():
         case = {"op": toks[0]}
         for t in toks[1:]:
             k, v = t.split("=")
-            case[k] = [int(x) for x in v.split(",")] if k == "ipiv" else (int(v) if k == "info" else _mat(v))
+            if k == "ipiv":
+                case[k] = [int(x) for x in v.split(",")]
+            elif k == "info":
+                case[k] = int(v)
+            elif k == "b" or (case["op"] == "potrs" and k == "expect"):
+                case[k] = np.array([float(x) for x in v.split(",")])
+            else:
+                case[k] = _mat(v)
         out.append(case)
     return out

@@ -59,6 +59,9 @@ def test_oracle_spec_linalg(case):
     elif case["op"] == "trsm_rltn":
         got = O.trsm_rltn(P(case["L"]), P(case["B"]))
         assert np.array_equal(O.to_f64_array(got), case["expect"])
+    elif case["op"] == "potrs":
+        l, info = O.potrf_lower(P(case["A"]))
+        assert np.array_equal(O.to_f64_array(O.potrs_lower(l, P(case["b"]))), case["expect"])
 
 
 # ---- the CUDA path against the same fixtures (values, not the oracle) --------
@@ -114,4 +117,11 @@ def test_gpu_golden_linalg(cuda_ok):
             B = dev(case["B"])
             PB.posit_trsm("R", "L", "T", "N", dev(case["L"]), B)
             assert np.array_equal(f64(B), case["expect"])
+        elif case["op"] == "potrs":
+            A = dev(case["A"])
+            info = torch.zeros(1, dtype=torch.int32, device="cuda")
+            PB.posit_potrf(A, info, nb=1)
+            b = dev(case["b"])
+            PB.posit_potrs(A, b)
+            assert np.array_equal(f64(b), case["expect"])
         to_host(torch.zeros(1, device="cuda"))

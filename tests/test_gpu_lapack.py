@@ -114,3 +114,40 @@ def test_potrf_not_positive_definite(cuda_ok):
     assert info == rinfo == 46
     # the blocks before the failing block are fully defined and bit-identical
     assert mismatch(np.tril(got)[:, :32], np.tril(ref)[:, :32]) == 0
+
+
+@pytest.mark.parametrize("n", [1, 33, 300])
+def test_getrs_potrs_match_oracle(cuda_ok, n):
+    import torch
+    import paper_2401_14117_b200 as PB
+    b = _pats(SI.normal_matrix((n,), 1.0, 7))
+    LU, piv, _ = O.getrf(_pats(SI.lu_matrix(n, 9)))
+    db = to_dev(b)
+    PB.posit_getrs(to_dev(LU), torch.from_numpy(piv).cuda(), db)
+    assert mismatch(to_host(db), O.getrs(LU, piv, b)) == 0
+    L, info = O.potrf_lower(_pats(SI.config3(n)))
+    assert info == 0
+    db = to_dev(b)
+    PB.posit_potrs(to_dev(L), db)
+    assert mismatch(to_host(db), O.potrs_lower(L, b)) == 0
+
+
+def test_getrs_full_size_backward_error(cuda_ok):
+    # configs[3] recipe at n = 4096 on the GPU factors: relative backward error (Eq.4,
+    # P:470-472) of the posit solve within the textbook gamma_n = n * eps bound,
+    # eps = 2^-27 (f_s = 27 near 1); S:241's 1e-6 is for n = 64
+    import torch
+    import paper_2401_14117_b200 as PB
+    n = 4096
+    A64 = SI.config4(n)
+    dA = PB.posit_from_f64(torch.from_numpy(A64).cuda())
+    ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    PB.posit_getrf(dA, ipiv, info, nb=256)
+    x_sol = np.full(n, 1.0 / np.sqrt(n))
+    b64 = A64 @ x_sol
+    db = PB.posit_from_f64(torch.from_numpy(b64).cuda())
+    PB.posit_getrs(dA, ipiv, db)
+    x = PB.posit_to_f64(db).cpu().numpy()
+    e = np.linalg.norm(b64 - A64 @ x) / np.linalg.norm(b64)
+    assert int(info.cpu()[0]) == 0 and e < n * 2.0 ** -27

@@ -264,3 +264,68 @@ def test_potrf_block_size_invariance():
         got, info = blocked_potrf_from_oracle_pieces(A, nb)
         assert info == rinfo == 0
         assert np.array_equal(np.tril(got), np.tril(ref))
+
+
+# ------------------------------------------------------------- solves -----
+# Rgetrs / Rpotrs of the accuracy study, reading Q21: reference
+# BLAS trsv loop order (forward: ascending k; back: descending k).
+def test_getrs_potrs_spec_examples():
+    b = P([4.0, 9.0])
+    L, info = O.potrf_lower(P(np.diag([4.0, 9.0])))
+    assert info == 0 and np.array_equal(F(O.potrs_lower(L, b)), [1.0, 1.0])
+    bb = P(SI.normal_matrix((6,), 1.0, 3))
+    assert np.array_equal(O.potrs_lower(P(np.eye(6)), bb), bb)                    # S:239 (L = I)
+    LU, ipiv, info = O.getrf(P(np.eye(6)))
+    assert np.array_equal(O.getrs(LU, ipiv, bb), bb)
+
+
+def test_getrs_dyadic_exact_with_pivots():
+    # P A = L U with dyadic L, U and an explicit row permutation; x small integers:
+    # every intermediate of both substitutions is exact, so x is recovered exactly
+    n = 16
+    L, U = _dyadic_lu(n, 21)
+    perm = np.random.default_rng(4).permutation(n)
+    A = (L @ U)[np.argsort(perm)]            # rows permuted: getrf must undo it
+    x = np.random.default_rng(5).integers(-4, 5, n).astype(np.float64)
+    LU, ipiv, info = O.getrf(P(A))
+    assert info == 0
+    got = F(O.getrs(LU, ipiv, P(A @ x)))
+    np.testing.assert_allclose(got, x, rtol=0, atol=1e-6)
+
+
+def _checker_back_desc(U, y):
+    # brute force with exact-rational ops in the Q21 order (descending k)
+    n = len(y)
+    y = [int(v) for v in y]
+    for i in range(n - 1, -1, -1):
+        for k in range(n - 1, i, -1):
+            y[i] = X.sub(y[i], X.mul(int(U[i, k]), y[k]))
+        y[i] = X.div(y[i], int(U[i, i]))
+    return y
+
+
+def _checker_fwd(L, b, unit):
+    n = len(b)
+    b = [int(v) for v in b]
+    for i in range(n):
+        for k in range(i):
+            b[i] = X.sub(b[i], X.mul(int(L[i, k]), b[k]))
+        if not unit:
+            b[i] = X.div(b[i], int(L[i, i]))
+    return b
+
+
+def test_getrs_potrs_match_checker_brute_force():
+    n = 7
+    A = P(SI.lu_matrix(n, 11))
+    b = P(SI.normal_matrix((n,), 1.0, 12))
+    LU, ipiv, _ = O.getrf(A)
+    pb = [int(v) for v in b]
+    for k, p in enumerate(ipiv):
+        pb[k], pb[p - 1] = pb[p - 1], pb[k]
+    y = _checker_fwd(LU, pb, unit=True)
+    assert list(O.getrs(LU, ipiv, b)) == _checker_back_desc(LU, y)
+    S = P(SI.config3(n))
+    Lc, _ = O.potrf_lower(S)
+    y = _checker_fwd(Lc, b, unit=False)
+    assert list(O.potrs_lower(Lc, b)) == _checker_back_desc(Lc.T.copy(), y)
