@@ -11,9 +11,10 @@ namespace pg {
 // Tile configuration.  One CTA = BM x BN outputs, NTHR threads, each thread a
 // TM x TN register tile of decoded accumulators; operands staged in k-slabs
 // of BK, double-buffered in shared memory as decoded (M, w) pairs.
-template <int BM_, int BN_, int TM_, int TN_, int MINB_>
+template <int BM_, int BN_, int TM_, int TN_, int MINB_, int EFF100 = 100>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = 16, MINB = MINB_;
+  static constexpr double EFF = EFF100 / 100.0;   // measured full-size rate relative to the 64 x 128 tile
   static constexpr int NTX = BN / TN, NTY = BM / TM, NTHR = NTX * NTY;
   static constexpr int AQN = BM * BK / 4, BQN = BN * BK / 4;    // quads per tile
   static constexpr int AQ = (AQN + NTHR - 1) / NTHR;            // A quads per thread (last may idle)
@@ -271,12 +272,11 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
 
 // ---- launchers (called from capi.cu) ----------------------------------------
 namespace {
-using V0 = pg::Cfg<64, 128, 8, 4, 1>;    // 256 thr, 32 accumulators / thread
-using V1 = pg::Cfg<64, 64, 4, 4, 2>;     // 256 thr, 16 acc, 2 CTAs / SM
-using V2 = pg::Cfg<64, 128, 4, 4, 1>;    // 512 thr, 16 acc
-using V3 = pg::Cfg<32, 128, 4, 4, 2>;    // 256 thr, 16 acc, 2 CTAs / SM
-using V4 = pg::Cfg<32, 128, 2, 4, 3>;    // 256 thr, 8 acc, 3 CTAs / SM
-using V5 = pg::Cfg<64, 128, 4, 8, 1>;    // 256 thr, 32 acc (TN = 8)
+// Tile configurations (all 16 decoded accumulators per thread, 128 registers)
+using V1 = pg::Cfg<64, 64, 4, 4, 2, 96>;     // 256 thr, 2 CTAs / SM
+using V2 = pg::Cfg<64, 128, 4, 4, 1, 100>;   // 512 thr, 1 CTA / SM: the big trailing updates
+using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // 256 thr, 2 CTAs / SM: short-and-wide (LU TRSM updates)
+using V6 = pg::Cfg<128, 32, 4, 4, 2, 97>;    // 256 thr, 2 CTAs / SM: tall-and-narrow (Cholesky TRSM updates)
 
 template <class C>
 int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
@@ -300,21 +300,47 @@ int variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("POSIT_GEMM_VARIANT");
-    v = e ? atoi(e) : 2;
+    v = e ? atoi(e) : 0;
   }
   return v;
 }
+
+// Modelled time of a launch with config C: the busiest SM runs ceil(tiles /
+// 148) CTAs of NTHR x 16 accumulators each; an SM with 512 resident threads
+// issues at the full rate, one with only 256 (a lone small CTA) at ~2/3 of it
+// (measured: tools/tune_gemm.py, tall-narrow and short-wide trailing shapes).
+template <class C>
+double model_time(int64_t m, int64_t n, bool syrk) {
+  const int64_t rb = (m + C::BM - 1) / C::BM, cb = (n + C::BN - 1) / C::BN;
+  int64_t tiles = rb * cb;
+  if (syrk) tiles = tiles / 2 + rb;                       // lower-triangle tiles (approx.)
+  const int64_t per_sm = (tiles + 147) / 148;
+  const int64_t resident = (per_sm < C::MINB ? per_sm : C::MINB) * C::NTHR;
+  const double rate = (resident >= 512 ? 1.0 : 0.66) * C::EFF;
+  return (double)per_sm * C::NTHR * 16.0 / rate;
+}
 }  // namespace
 
+// Picks the tile shape with the smallest modelled time for this problem;
+// near-ties (within 10%) go to the 64 x 128 tile.  All configurations compute the same
+// bits (same per-element order), so the choice is performance only.
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   if (P.m == 0 || P.n == 0) return 0;
-  switch (variant()) {
+  int v = variant();
+  if (v == 0) {
+    const double w2 = model_time<V2>(P.m, P.n, syrk), w1 = model_time<V1>(P.m, P.n, syrk);
+    const double w3 = model_time<V3>(P.m, P.n, syrk), w6 = model_time<V6>(P.m, P.n, syrk);
+    v = 2;
+    double best = w2;
+    if (w1 < best * 0.9) { v = 1; best = w1; }
+    if (w3 < best * 0.9) { v = 3; best = w3; }
+    if (w6 < best * 0.9) { v = 6; best = w6; }
+  }
+  switch (v) {
     case 1: return launch_cfg<V1>(P, transb, syrk, st);
-    case 2: return launch_cfg<V2>(P, transb, syrk, st);
     case 3: return launch_cfg<V3>(P, transb, syrk, st);
-    case 4: return launch_cfg<V4>(P, transb, syrk, st);
-    case 5: return launch_cfg<V5>(P, transb, syrk, st);
-    default: return launch_cfg<V0>(P, transb, syrk, st);
+    case 6: return launch_cfg<V6>(P, transb, syrk, st);
+    default: return launch_cfg<V2>(P, transb, syrk, st);
   }
 }
 

@@ -120,29 +120,52 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& hi, ui
   asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%1, %0}, w;\n\t}" : "=r"(hi), "=r"(lo) : "r"(a), "r"(b));
 }
 
+
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 
+// Table access for the GEMM: the two shared-memory tables.
 struct MacConst {
   uint32_t one, sixteen;               // = 1, 16 at run time (opaque to ptxas)
   uint32_t tp0, tx0;                   // shared-memory byte addresses of table entry E = 0 (tx: Ex + 30 = 0)
+  __device__ __forceinline__ uint4 prod(int32_t Ep) const { return lds128(fmad((uint32_t)Ep, sixteen, tp0)); }
+  __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(fmad(Exi, sixteen, tx0)); }
+};
+
+// The same constants computed in registers (no shared-memory tables): used by
+// the panel-side kernels, where latency rather than issue rate matters.
+struct CalcConst {
+  uint32_t one = 1u;
+  __device__ __forceinline__ uint4 prod(int32_t Ep) const {
+    uint32_t t = (uint32_t)(Ep ^ (Ep >> 31)) >> 2;
+    t = t < (uint32_t)T_FAST_MAX ? t : (uint32_t)T_FAST_MAX;
+    return make_uint4(1u << (30 - t), 0u - (1u << (29 - t)), 1u << (t + 3), 0u);
+  }
+  __device__ __forceinline__ uint4 sum(uint32_t Exi) const {
+    const int32_t E = (int32_t)Exi - 30;
+    const uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
+    const bool fast = t <= (uint32_t)T_FAST_MAX;
+    const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;
+    return make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, 0u);
+  }
 };
 
 // ---- the decoded-domain MAC -------------------------------------------------
 // c <- c (+) (a (x) b), a = (Ma hidden@31, Ea, sa), b = (Mb hidden@30, Eb, sb),
 // signs as +1/-1 ints.  badacc accumulates BAD_FLAG when the sum leaves the
 // fast range (the caller checks it once per k-slab).
+template <class Tab>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
-                                    const MacConst& K, uint32_t& badacc) {
+                                    const Tab& K, uint32_t& badacc) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
   uint32_t hi, lo;
   mulwide(Ma, Mb, hi, lo);                            // hi in [2^29, 2^31)
   const uint32_t n = hi >> 30;
   const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
-  const uint4 T = lds128(fmad((uint32_t)Ep, K.sixteen, K.tp0));
+  const uint4 T = K.prod(Ep);
   // drop D = t + 2 + n bits of hi: hi * 2^(32 - D) splits into q (high) and the dropped bits (low, left-aligned)
   uint32_t qp, yp;
   mulwide(hi, fmad(n, T.y, T.x), qp, yp);
@@ -175,7 +198,7 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   asm("bfind.u32 %0, %1;" : "=r"(flo) : "r"(x));             // leading one (0xFFFFFFFF if x == 0)
   const uint32_t xf = __funnelshift_r(0u, x, flo);            // fraction bits left-aligned (hidden dropped)
   const uint32_t Exi = fmad(flo, K.one, (uint32_t)Ebg);       // Ex + 30
-  const uint4 U = lds128(fmad(Exi, K.sixteen, K.tx0));
+  const uint4 U = K.sum(Exi);
   uint32_t qx, yx;
   mulwide(xf, U.x, qx, yx);                                   // f_s fraction bits | the rest, left-aligned
   uint32_t rx;

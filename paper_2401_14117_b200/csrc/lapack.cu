@@ -136,18 +136,118 @@ __global__ void k_leaf_update(uint32_t* A, int64_t lda, int64_t m, int64_t w, in
   if (threadIdx.x == 0 && best != 0ull) atomicMax(&ws->key[j + 1], best);
 }
 
-// rows k1..k2-1 swapped with ipiv[k]-1-base, in order, for columns [0, ncols)
-__global__ void k_laswp(uint32_t* A, int64_t lda, int64_t ncols, int64_t k1, int64_t k2, const int32_t* ipiv,
-                        int64_t base) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncols) return;
-  for (int64_t k = k1; k < k2; k++) {
-    const int64_t r2 = (int64_t)ipiv[k] - 1 - base;
-    if (r2 != k) {
-      const uint32_t t = A[k * lda + c];
-      A[k * lda + c] = A[r2 * lda + c];
-      A[r2 * lda + c] = t;
+// laswp: rows k1..k2-1 swapped with ipiv[k]-1-base, in order, on columns
+// [0, ncols).  One CTA per 32 columns.  Instead of walking the swaps through
+// global memory (a dependent load/store chain per swap), the CTA gathers every
+// row the swaps touch into shared memory (the k2-k1 rows themselves plus each
+// distinct pivot row), applies the swaps there in order, and scatters the rows
+// back: the global traffic is independent loads and stores.
+constexpr int SWP_MAX = 256;   // swaps per pass (longer ranges run in passes)
+constexpr int SWP_COLS = 32;
+
+__global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t ncols, int64_t k1, int64_t k2,
+                                               const int32_t* ipiv, int64_t base) {
+  extern __shared__ uint32_t swp_smem[];
+  uint32_t (*val)[SWP_COLS] = reinterpret_cast<uint32_t (*)[SWP_COLS]>(swp_smem);   // [2 * SWP_MAX][SWP_COLS]
+  __shared__ int32_t tgt[SWP_MAX];      // pivot row of swap s (relative row index)
+  __shared__ int16_t slot[SWP_MAX];     // slot holding that row
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * SWP_COLS + lane;
+  for (int64_t s0 = k1; s0 < k2; s0 += SWP_MAX) {
+    const int ns = (int)((k2 - s0) < SWP_MAX ? (k2 - s0) : SWP_MAX);
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) tgt[s] = ipiv[s0 + s] - 1 - (int32_t)base;
+    __syncthreads();
+    // slot of each pivot row: inside the block -> its own row slot; outside ->
+    // the slot of its first occurrence (ns + index), so repeated pivots share it
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+      const int32_t p = tgt[s];
+      int sl;
+      if (p >= s0 && p < s0 + ns) {
+        sl = (int)(p - s0);
+      } else {
+        int f = s;
+        for (int t = 0; t < s; t++)
+          if (tgt[t] == p) { f = t; break; }
+        sl = ns + f;
+      }
+      slot[s] = (int16_t)sl;
     }
+    __syncthreads();
+    // gather
+    for (int s = wid; s < ns; s += nw) {
+      val[s][lane] = c < ncols ? A[(s0 + s) * lda + c] : 0u;
+      if (slot[s] == ns + s) val[ns + s][lane] = c < ncols ? A[(int64_t)tgt[s] * lda + c] : 0u;
+    }
+    __syncthreads();
+    // swaps in order (warp 0, lane = column)
+    if (wid == 0) {
+      for (int s = 0; s < ns; s++) {
+        const int q = slot[s];
+        if (q != s) {
+          const uint32_t t = val[s][lane];
+          val[s][lane] = val[q][lane];
+          val[q][lane] = t;
+        }
+      }
+    }
+    __syncthreads();
+    // scatter
+    for (int s = wid; s < ns; s += nw) {
+      if (c < ncols) {
+        A[(s0 + s) * lda + c] = val[s][lane];
+        if (slot[s] == ns + s) A[(int64_t)tgt[s] * lda + c] = val[ns + s][lane];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- decoded lane values for the in-block kernels -----------------------------
+// A value that lives in a register across many posit updates is kept decoded
+// (the GEMM's accumulator format, csrc/gemm.cuh) so that each update
+// c <- c (-) a (x) b runs the decoded-domain MAC (one rounding for the product,
+// one for the difference, as always) instead of decode -> mul -> encode ->
+// decode -> sub -> encode.  Conservative range guards route any update whose
+// operands or result could leave the MAC's exact range (zero / NaR operands,
+// |E| > 37 operands, |E| > 75 values) to the generic pattern path; both are
+// bit-identical by construction.
+struct LaneVal {
+  pg::Acc a;       // decoded (valid when dec)
+  uint32_t pat;    // pattern (valid when !dec)
+  bool dec;
+};
+
+__device__ __forceinline__ void lv_load(LaneVal& v, uint32_t x) {
+  v.pat = x;
+  v.dec = pg::acc_decode(x, v.a) && (x == 0u || (v.a.E <= 75 && v.a.E >= -75));
+}
+
+__device__ __forceinline__ uint32_t lv_pattern(const LaneVal& v) { return v.dec ? pg::acc_encode(v.a) : v.pat; }
+
+// operand view of a lane value: B format (hidden@30), fast iff nonzero and |E| <= 37
+__device__ __forceinline__ bool lv_operand(const LaneVal& v) {
+  return v.dec && v.a.E > -1000 && v.a.E <= 37 && v.a.E >= -37;
+}
+
+// A-format decode of a pattern operand: fast iff nonzero, not NaR, |E| <= 37
+__device__ __forceinline__ bool fast_a(uint32_t x, uint4& d) {
+  uint32_t sp = 0u;
+  d = pg::stage_decode<31>(x, 0u, sp);
+  return sp == 0u && (int32_t)d.y <= 37 && (int32_t)d.y >= -37;
+}
+
+// c <- c (-) a (x) b; a = pattern (with its A-format decode), b = operand lane
+// value broadcast as (M, E, sg) plus its pattern bp.
+__device__ __forceinline__ void lv_fms(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
+                                       int32_t bsg, bool bfast, uint32_t bp) {
+  if (afast && bfast && c.dec) {
+    uint32_t bad = 0u;
+    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, pg::CalcConst(), bad);
+    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
+    if (!c.dec) c.pat = pg::acc_encode(c.a);                 // |E| in (75, 107]: exact, leave the fast range
+  } else {
+    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
+    lv_load(c, r);
   }
 }
 
@@ -167,69 +267,119 @@ __global__ void __launch_bounds__(1024) k_trsm_llnu_blk(const uint32_t* L, int64
     sb[wid][lane] = (c0 + lane < n) ? B[(i0 + wid) * ldb + c0 + lane] : 0u;
   }
   __syncthreads();
-  uint32_t b = lane < ib ? sb[lane][wid] : 0u;
+  LaneVal b;
+  lv_load(b, lane < ib ? sb[lane][wid] : 0u);
   for (int k = 0; k < ib - 1; k++) {
-    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, b, k);
-    if (lane > k && lane < ib) b = sub(b, mul(sl[lane][k], bk));
+    const bool bf = lv_operand(b);
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, k);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, k);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, k);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, k) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, lane == k ? lv_pattern(b) : 0u, k);   // for the generic path
+    if (lane > k && lane < ib) {
+      const uint32_t ap = sl[lane][k];
+      uint4 ad;
+      const bool af = fast_a(ap, ad);
+      lv_fms(b, ap, af, ad, bM, bE, bs, bfk, bpk);
+    }
   }
-  if (lane < ib) sb[lane][wid] = b;
+  if (lane < ib) sb[lane][wid] = lv_pattern(b);
   __syncthreads();
   if (wid < ib && c0 + lane < n) B[(i0 + wid) * ldb + c0 + lane] = sb[wid][lane];
 }
 
-// Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 32).
-// Warp per row of B, lane = column (coalesced): step k finalises b_k <- b_k (/)
-// l_kk, broadcasts it, and columns j > k apply b_j <- b_j (-) b_k (x) l_jk.
+// Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 16).
+// Half-warp per row of B (two rows per warp), lane = column (coalesced):
+// step k finalises b_k <- b_k (/) l_kk, broadcasts it within the half-warp,
+// and columns j > k apply b_j <- b_j (-) b_k (x) l_jk (ascending k).
+constexpr int TBR = 16;
+
 __global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
                                                         int64_t j0, int64_t jb, int64_t m, const int32_t* stop) {
-  __shared__ uint32_t sl[TB][TB + 1];
+  __shared__ uint32_t sl[TBR][TBR + 1];
   if (stop != nullptr && *stop != 0) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid < jb) sl[wid][lane] = lane <= wid ? L[(j0 + wid) * ldl + j0 + lane] : 0u;
-  __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * 32 + wid;
-  if (r >= m) return;
-  uint32_t b = lane < jb ? B[r * ldb + j0 + lane] : 0u;
-  for (int k = 0; k < jb; k++) {
-    if (lane == k) b = div(b, sl[k][k]);
-    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, b, k);
-    if (lane > k && lane < jb) b = sub(b, mul(bk, sl[lane][k]));
+  const int col = lane & (TBR - 1), half = lane & TBR;
+  if (threadIdx.x < TBR * TBR) {
+    const int rr = threadIdx.x / TBR, cc = threadIdx.x % TBR;
+    if (rr < jb) sl[rr][cc] = cc <= rr ? L[(j0 + rr) * ldl + j0 + cc] : 0u;
   }
-  if (lane < jb) B[r * ldb + j0 + lane] = b;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * 64 + wid * 2 + (half ? 1 : 0);
+  if ((int64_t)blockIdx.x * 64 + wid * 2 >= m) return;          // whole warp out of range
+  const bool live = r < m && col < jb;
+  LaneVal b;
+  lv_load(b, live ? B[r * ldb + j0 + col] : 0u);
+  for (int k = 0; k < jb; k++) {
+    if (col == k && live) lv_load(b, div(lv_pattern(b), sl[k][k]));
+    const bool bf = lv_operand(b);
+    const int src = half | k;
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, src);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, src);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, src);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, src) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, col == k ? lv_pattern(b) : 0u, src);   // for the generic path
+    if (live && col > k) {
+      const uint32_t ap = sl[col][k];
+      uint4 ad;
+      const bool af = fast_a(ap, ad);
+      lv_fms(b, ap, af, ad, bM, bE, bs, bfk, bpk);
+    }
+  }
+  if (live) B[r * ldb + j0 + col] = lv_pattern(b);
 }
 
-// ---- Cholesky leaf: b <= 32 diagonal block in shared memory, one CTA ---------
+// ---- Cholesky leaf: b <= 32 diagonal block, one CTA, thread (i, j) owns a_ij --
 // Textbook loop (reading Q9): for k: if signed(a_kk) <= 0 -> info = k+1, stop;
 // a_kk <- sqrt(a_kk); a_ik <- a_ik (/) a_kk; a_ij <- a_ij (-) a_ik (x) a_jk.
+// Warp = column j, lane = row i, so the divisions of step k are one warp's
+// work; column k is published through shared memory as patterns plus decoded
+// operands, and each thread keeps its element decoded across the k loop.
 __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, int64_t b, int32_t* info,
                                                      int64_t row_base) {
-  __shared__ uint32_t s[TB][TB + 1];
+  __shared__ uint32_t colp[TB];          // column k patterns
+  __shared__ uint4 cola[TB];             // column k, A-format decode (hidden@31) + fast flag in .w
+  __shared__ uint4 colb[TB];             // column k, B-format decode (hidden@30) + fast flag in .w
   __shared__ int fail;
   if (*info != 0) return;                                  // an earlier block failed: stop
-  const int i = threadIdx.x >> 5, j = threadIdx.x & 31;    // row, column
-  const bool in = i < b && j <= i;
-  if (in) s[i][j] = A[i * lda + j];
+  const int j = threadIdx.x >> 5, i = threadIdx.x & 31;    // column (warp), row (lane)
+  const bool in = i < b && j <= i && j < b;
+  LaneVal v;
+  lv_load(v, in ? A[i * lda + j] : 0u);
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
   int k = 0;
   for (; k < b; k++) {
-    if (threadIdx.x == 0) {
-      const uint32_t v = s[k][k];
-      if ((int32_t)v <= 0) {                               // zero, negative or NaR pivot
-        fail = 1;
-        *info = (int32_t)(row_base + k + 1);
-      } else {
-        s[k][k] = p32::sqrt(v);
+    if (j == k) {                                          // warp k: pivot, then the column's divisions
+      uint32_t d = 0u;
+      if (i == k) {
+        d = lv_pattern(v);
+        if ((int32_t)d > 0) {
+          lv_load(v, p32::sqrt(d));
+          d = lv_pattern(v);
+        }
+      }
+      d = __shfl_sync(0xFFFFFFFFu, d, k);
+      if ((int32_t)d <= 0) {                               // zero, negative or NaR pivot
+        if (i == k) { fail = 1; *info = (int32_t)(row_base + k + 1); }
+      } else if (in && i > k) {
+        lv_load(v, div(lv_pattern(v), d));
+        const uint32_t x = lv_pattern(v);
+        colp[i] = x;
+        uint4 ad;
+        cola[i] = fast_a(x, ad) ? make_uint4(ad.x, ad.y, ad.z, 1u) : make_uint4(0u, 0u, 0u, 0u);
+        colb[i] = lv_operand(v) ? make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)v.a.sg, 1u) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
     __syncthreads();
     if (fail) break;
-    if (j == k && i > k && i < b) s[i][k] = div(s[i][k], s[k][k]);
-    __syncthreads();
-    if (in && j > k) s[i][j] = sub(s[i][j], mul(s[i][k], s[j][k]));
+    if (in && j > k) {
+      const uint4 ad = cola[i], bd = colb[j];
+      lv_fms(v, colp[i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, colp[j]);
+    }
     __syncthreads();
   }
-  if (in) A[i * lda + j] = s[i][j];
+  if (in) A[i * lda + j] = lv_pattern(v);
 }
 
 // ---- one-RHS solves for the accuracy report (Rgetrs / Rpotrs) -----
@@ -394,8 +544,14 @@ int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv
 int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv, int64_t ipiv_base,
              cudaStream_t st) {
   if (ncols <= 0 || k2 <= k1) return 0;
+  constexpr size_t smem = 2 * SWP_MAX * SWP_COLS * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_laswp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   pb_count_launch();
-  k_laswp<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(A, lda, ncols, k1, k2, ipiv, ipiv_base);
+  k_laswp<<<(unsigned)((ncols + SWP_COLS - 1) / SWP_COLS), 256, smem, st>>>(A, lda, ncols, k1, k2, ipiv, ipiv_base);
   return last_launch();
 }
 
@@ -420,10 +576,10 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
 int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, const int32_t* stop,
                  cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
-  for (int64_t j0 = 0; j0 < n; j0 += TB) {
-    const int64_t jb = (n - j0) < TB ? (n - j0) : TB;
+  for (int64_t j0 = 0; j0 < n; j0 += TBR) {
+    const int64_t jb = (n - j0) < TBR ? (n - j0) : TBR;
     pb_count_launch();
-    k_trsm_rltn_blk<<<(unsigned)((m + 31) / 32), 1024, 0, st>>>(L, ldl, B, ldb, j0, jb, m, stop);
+    k_trsm_rltn_blk<<<(unsigned)((m + 63) / 64), 1024, 0, st>>>(L, ldl, B, ldb, j0, jb, m, stop);
     if (j0 + jb < n) {
       // B[:, j0+jb:] -= B[:, j0:j0+jb] * L[j0+jb:, j0:j0+jb]^T   (NT GEMM, K = jb)
       pg::Params P{m, n - j0 - jb, jb, B + j0, ldb, L + (j0 + jb) * ldl + j0, ldl, B + j0 + jb, ldb, 1, 1, stop};

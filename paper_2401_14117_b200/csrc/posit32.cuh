@@ -114,9 +114,14 @@ __device__ __forceinline__ uint32_t div(uint32_t a, uint32_t b) {
   if (a == NAR || b == NAR || b == 0u) return NAR;  // reading Q3
   if (a == 0u) return 0u;
   const Dec x = decode(a), y = decode(b);
+  // q = floor(Mx 2^32 / My), r = remainder: estimate with one correctly rounded
+  // binary64 division (both operands exact in binary64; |estimate - quotient|
+  // < 1), then fix q by the sign / size of the exact 64-bit remainder.
   const uint64_t num = (uint64_t)x.M << 32;
-  uint64_t q = num / y.M;                            // in (2^31, 2^33)
-  const uint64_t r = num - q * y.M;
+  uint64_t q = (uint64_t)__ddiv_rn((double)x.M * 4294967296.0, (double)y.M);
+  int64_t r = (int64_t)(num - q * (uint64_t)y.M);
+  if (r < 0) { q -= 1u; r += (int64_t)y.M; }
+  else if (r >= (int64_t)y.M) { q += 1u; r -= (int64_t)y.M; }
   int32_t E = x.E - y.E;
   int lz = __clzll((long long)q);                    // 31 (q >= 2^32) or 32
   E += 31 - lz;                                      // leading one at bit 32 -> E, at 31 -> E-1

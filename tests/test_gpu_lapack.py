@@ -151,3 +151,57 @@ def test_getrs_full_size_backward_error(cuda_ok):
     x = PB.posit_to_f64(db).cpu().numpy()
     e = np.linalg.norm(b64 - A64 @ x) / np.linalg.norm(b64)
     assert int(info.cpu()[0]) == 0 and e < n * 2.0 ** -27
+
+
+@pytest.mark.parametrize("scale", [-90, -40, 0, 40, 90])
+def test_trsm_extreme_scales_and_zeros(cuda_ok, scale):
+    # magnitudes outside the decoded fast range (|E| > 37 / 75) and exact zeros
+    # force the in-block kernels' generic fallback path on some lanes
+    import paper_2401_14117_b200 as PB
+    m, n = 70, 90
+    L64 = np.tril(SI.lu_matrix(m, 13), -1) + np.eye(m)
+    L64[5:9, 1:4] = 0.0
+    B64 = np.ldexp(SI.normal_matrix((m, n), 1.0, 14), scale)
+    B64[:, 7] = 0.0
+    B64[10, :] = 0.0
+    L, B = _pats(L64), _pats(B64)
+    dB = to_dev(B)
+    PB.posit_trsm("L", "L", "N", "U", to_dev(L), dB)
+    assert mismatch(to_host(dB), O.trsm_llnu(L, B)) == 0
+    Lr64 = np.tril(np.ldexp(SI.lu_matrix(n, 15), scale // 2), -1) + np.diag(np.ldexp(1.0 + np.arange(n) % 5, scale // 2))
+    Lr64[20:25, 3:6] = 0.0
+    Lr = _pats(Lr64)
+    Br = _pats(np.ldexp(SI.normal_matrix((m, n), 1.0, 16), scale))
+    dB = to_dev(Br)
+    PB.posit_trsm("R", "L", "T", "N", to_dev(Lr), dB)
+    assert mismatch(to_host(dB), O.trsm_rltn(Lr, Br)) == 0
+
+
+@pytest.mark.parametrize("scale", [-100, -60, 60, 100])
+def test_potrf_extreme_scales(cuda_ok, scale):
+    n = 100
+    A = _pats(np.ldexp(SI.config3(n), scale))
+    got, ginfo = _gpu_potrf(A, 32)
+    ref, rinfo = O.potrf_lower(A)
+    il = np.tril_indices(n)
+    assert ginfo == rinfo and mismatch(got[il], ref[il]) == 0
+
+
+@pytest.mark.parametrize("ncols,k1,k2", [(1, 0, 5), (45, 3, 40), (300, 10, 300), (77, 0, 600)])
+def test_laswp_sequential_semantics(cuda_ok, ncols, k1, k2):
+    # pure data movement: swaps applied in order, repeated and in-block pivots
+    import torch
+    import paper_2401_14117_b200 as PB
+    m = 900
+    rng = np.random.default_rng(k2)
+    A = rng.integers(0, 2 ** 32, (m, ncols), dtype=np.uint64).astype(np.uint32)
+    ipiv = np.arange(1, m + 1, dtype=np.int32)
+    for k in range(k1, k2):
+        ipiv[k] = rng.choice([k + 1, rng.integers(k + 1, m + 1), rng.integers(k1 + 1, k2 + 1), 7 * k2 % m + 1])
+    ref = A.copy()
+    for k in range(k1, k2):
+        p = ipiv[k] - 1
+        ref[[k, p]] = ref[[p, k]]
+    dA = to_dev(A)
+    PB.posit_laswp(dA, k1, k2, torch.from_numpy(ipiv).cuda())
+    assert mismatch(to_host(dA), ref) == 0
