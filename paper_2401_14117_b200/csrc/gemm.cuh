@@ -216,4 +216,42 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   badacc = fmad(U.z, K.one, badacc);                          // BAD_FLAG bits accumulate
 }
 
+// ---- decoded-domain division -----------------------------------------------
+// x <- x (/) y, correctly rounded, for a nonzero divisor y = (My hidden@30, Ey,
+// sy) with rcp = RN(2^32 / My) (binary64, shared by every dividend).  The
+// quotient of the significands comes from one binary64 product, exact to +-1,
+// fixed by the exact 64-bit remainder; it is then rounded at f_s like a sum.
+// Returns false (x unchanged) when the result could leave |E| <= 107.
+template <class Tab>
+__device__ __forceinline__ bool acc_div(Acc& x, uint32_t My, int32_t Ey, int32_t sy, double rcp, const Tab& K) {
+  if (x.E < E_ZERO_LIMIT) return true;                         // 0 / y = 0
+  const int32_t de = x.E - Ey;
+  if (de > 105 || de < -105) return false;
+  const uint64_t num = (uint64_t)x.M << 32;
+  uint64_t q = (uint64_t)((double)x.M * rcp);
+  int64_t r = (int64_t)(num - q * (uint64_t)My);
+  if (r < 0) { q -= 1u; r += (int64_t)My; }
+  else if (r >= (int64_t)My) { q += 1u; r -= (int64_t)My; }
+  uint32_t st = r != 0 ? 1u : 0u;
+  int32_t E = de - 1;                                          // q in (2^31, 2^33): hidden bit at 31 or 32
+  if (q >> 32) { st |= (uint32_t)q & 1u; q >>= 1; E += 1; }
+  const uint32_t xf = (uint32_t)q << 1;                        // fraction left-aligned
+  const uint4 U = K.sum((uint32_t)(E + 30));
+  if (U.z != 0u) return false;
+  uint32_t qx, yx;
+  mulwide(xf, U.x, qx, yx);
+  uint32_t rx;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %1, 0xFFFFFFFF;\n\t"                      // CF = sticky
+      "addc.cc.u32 t, %2, 0x7FFFFFFF;\n\t"                     // CF = round up (RNE)
+      "addc.u32 %0, %3, %4;\n\t}"                               // + hidden bit
+      : "=r"(rx) : "r"(st), "r"(yx | (qx & 1u)), "r"(qx), "r"(U.x));
+  const uint32_t Mn = rx * U.y;
+  const uint32_t cy = Mn >> 31;
+  x.M = Mn >> cy;
+  x.E = E + (int32_t)cy;
+  x.sg = x.sg * sy;
+  return true;
+}
+
 }  // namespace pg

@@ -251,6 +251,21 @@ __device__ __forceinline__ void lv_fms(LaneVal& c, uint32_t ap, bool afast, cons
   }
 }
 
+// lv_fms with the GEMM's shared-memory tables (or any table type)
+template <class Tab>
+__device__ __forceinline__ void lv_fms_t(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
+                                         int32_t bsg, bool bfast, uint32_t bp, const Tab& K) {
+  if (afast && bfast && c.dec) {
+    uint32_t bad = 0u;
+    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, K, bad);
+    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
+    if (!c.dec) c.pat = pg::acc_encode(c.a);
+  } else {
+    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
+    lv_load(c, r);
+  }
+}
+
 // ---- TRSM in-block kernels (32-wide, right-looking across a warp) -----------
 // Unit lower, left: rows i0..i0+ib-1 of B (ib <= 32).  CTA = 32 warps = 32
 // columns; the 32 x 32 tile goes through shared memory (coalesced); warp w
@@ -327,6 +342,170 @@ __global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64
     }
   }
   if (live) B[r * ldb + j0 + col] = lv_pattern(b);
+}
+
+// ---- fused right TRSM (Cholesky L21 = A21 L11^-T), n <= 256 ----------------
+// Rows of B are independent, so one CTA solves FR_ROWS whole rows: B's tile
+// lives in shared memory (patterns); per W-column block J a group of W lanes
+// per row runs the in-block substitution (lane = column, as k_trsm_rltn_blk),
+// publishes the block's W final values decoded, and every thread then updates
+// its own columns of the later blocks with them (the fast MAC with the
+// GEMM's shared-memory constant tables; L's block column staged decoded,
+// k-major so a lane group reads consecutive words).  Per element the updates
+// still arrive one at a time in ascending k (Q6).
+constexpr int FR_ROWS = 32, FR_NMAX = 256, FR_W = 16;
+
+template <int W>
+struct FrSmem {
+  uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
+  uint4 ld[W][FR_NMAX];                       // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
+  uint4 bop[FR_ROWS][W];                      // block J's final values, B-format {M, E, sg (0: slow), pattern}
+  uint32_t lblk[W][W + 1];                    // L's diagonal block J (patterns)
+  uint4 lblkd[W][W];                          // the same, decoded A-format {M, E, sigma, fast}
+  uint4 ldiag[W];                             // L[c0 + k][c0 + k] as a divisor {M hidden@30, E, sg, fast}
+  double ldrcp[W];                            // RN(2^32 / M) of each diagonal divisor
+  int colfast[FR_NMAX];                       // column j's staged L values all fast-path operands
+  int rowfast[FR_ROWS];                       // row r's block-J values all fast-path operands
+  uint4 tp[pg::TSIZE];                        // the MAC's per-scale constant tables
+  uint4 tx[pg::TSIZE];
+};
+
+template <int W>
+__global__ void __launch_bounds__(FR_ROWS * W) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
+                                                                 int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
+                                                                 int one) {
+  constexpr int NT = FR_ROWS * W;
+  extern __shared__ __align__(16) unsigned char fr_raw[];
+  FrSmem<W>& S = *reinterpret_cast<FrSmem<W>*>(fr_raw);
+  if (stop != nullptr && *stop != 0) return;
+  const int tid = threadIdx.x;
+  const int r = tid / W, c = tid % W;                  // row of the tile, column within a block
+  const int grp = (tid & 31) & ~(W - 1);               // first lane of this row's lane group
+  const int64_t r0 = (int64_t)blockIdx.x * FR_ROWS;
+  const int64_t rows = (m - r0) < FR_ROWS ? (m - r0) : FR_ROWS;
+  pg::fill_tables(S.tp, S.tx, tid, NT);
+  pg::MacConst K;
+  K.one = (uint32_t)one; K.sixteen = 16u * K.one;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
+  for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
+    const int rr = e / (int)n, cc = e % (int)n;
+    S.b[rr][cc] = rr < rows ? B[(r0 + rr) * ldb + cc] : 0u;
+  }
+  const int nblk = (int)((n + W - 1) / W);
+  for (int J = 0; J < nblk; J++) {
+    const int c0 = J * W;
+    const int jb = (int)((n - c0) < W ? (n - c0) : W);
+    __syncthreads();
+    // stage: L's diagonal block J (patterns) and L[j][c0 + k] for j >= c0 + jb (decoded)
+    for (int e = tid; e < W * W; e += NT) {
+      const int rr = e / W, cc = e % W;
+      if (rr < jb && cc <= rr) {
+        const uint32_t x = L[(c0 + rr) * ldl + c0 + cc];
+        S.lblk[rr][cc] = x;
+        uint4 d;
+        const bool f = fast_a(x, d);
+        S.lblkd[rr][cc] = make_uint4(d.x, d.y, d.z, f ? 1u : 0u);
+        if (rr == cc) {
+          pg::Acc a;
+          const bool ok = pg::acc_decode(x, a) && x != 0u && a.E <= 37 && a.E >= -37;
+          S.ldiag[rr] = make_uint4(a.M, (uint32_t)a.E, (uint32_t)a.sg, ok ? 1u : 0u);
+          S.ldrcp[rr] = ok ? __drcp_rn((double)a.M) * 4294967296.0 : 0.0;
+        }
+      }
+    }
+    const int nrest = (int)n - c0 - jb;
+    for (int jj = tid; jj < nrest; jj += NT) {            // thread per column j: its jb values are contiguous
+      const int j = c0 + jb + jj;
+      int f = 1;
+      for (int k = 0; k < jb; k++) {
+        const uint32_t x = L[(int64_t)j * ldl + c0 + k];
+        uint4 d;
+        const bool fk = fast_a(x, d);
+        S.ld[k][j] = make_uint4(d.x, d.y, d.z, x);
+        f &= (int)fk;
+      }
+      S.colfast[j] = f;
+    }
+    __syncthreads();
+    // in-block substitution: W lanes per row, lane = column
+    {
+      const bool live = r < rows && c < jb;
+      LaneVal v;
+      lv_load(v, live ? S.b[r][c0 + c] : 0u);
+      for (int k = 0; k < jb; k++) {
+        if (c == k && live) {
+          const uint4 dv = S.ldiag[k];
+          bool done = false;
+          if (v.dec && dv.w != 0u) done = pg::acc_div(v.a, dv.x, (int32_t)dv.y, (int32_t)dv.z, S.ldrcp[k], K);
+          if (done) {
+            if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
+          } else {
+            lv_load(v, div(lv_pattern(v), S.lblk[k][k]));
+          }
+        }
+        const bool bf = lv_operand(v);
+        const int src = grp | k;
+        const uint32_t bM = __shfl_sync(0xFFFFFFFFu, v.a.M, src);
+        const int32_t bE = __shfl_sync(0xFFFFFFFFu, v.a.E, src);
+        const int32_t bs = __shfl_sync(0xFFFFFFFFu, v.a.sg, src);
+        const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, src) != 0;
+        const bool bdk = __shfl_sync(0xFFFFFFFFu, (int)v.dec, src) != 0;
+        const uint32_t bpraw = __shfl_sync(0xFFFFFFFFu, v.pat, src);
+        if (live && c > k) {
+          const uint4 ad = S.lblkd[c][k];
+          if (ad.w != 0u && bfk && v.dec) {
+            uint32_t bad = 0u;
+            pg::mac(v.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bs, K, bad);
+            if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
+          } else {
+            pg::Acc bk{bM, bE, bs};
+            const uint32_t bp = bdk ? pg::acc_encode(bk) : bpraw;        // b_k's pattern (rare path)
+            lv_load(v, sub(lv_pattern(v), mul(S.lblk[c][k], bp)));
+          }
+        }
+      }
+      const bool opf = lv_operand(v) || !live;
+      const unsigned grpmask = (W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u)) << grp;
+      const bool allf = (__ballot_sync(0xFFFFFFFFu, opf) & grpmask) == grpmask;
+      if (live) {
+        const uint32_t x = lv_pattern(v);
+        S.b[r][c0 + c] = x;
+        S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), x);   // sign pre-negated: c (-) a b
+      }
+      if (c == 0) S.rowfast[r] = allf ? 1 : 0;
+    }
+    __syncthreads();
+    // updates of the later blocks: thread (r, c) owns columns c0 + jb + c + W t.
+    // A column whose k-loop has only fast operands and an accumulator within
+    // |E| <= 75 stays inside the MAC's exact range for all jb <= 16 steps
+    // (|Ep| <= 75, |E| grows by <= 1 per step, cancellation stops at >= -106).
+    if (r < rows) {
+      const bool rf = S.rowfast[r] != 0;
+      for (int col = c0 + jb + c; col < (int)n; col += W) {
+        uint32_t x = S.b[r][col];
+        pg::Acc a;
+        const bool ok = pg::acc_decode(x, a) && (x == 0u || (a.E <= 75 && a.E >= -75));
+        if (rf && ok && S.colfast[col] != 0) {
+          uint32_t bad = 0u;
+#pragma unroll 4
+          for (int k = 0; k < jb; k++) {
+            const uint4 ad = S.ld[k][col], bd = S.bop[r][k];
+            pg::mac(a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x, (int32_t)bd.y, (int32_t)bd.z, K, bad);
+          }
+          x = pg::acc_encode(a);
+        } else {
+          for (int k = 0; k < jb; k++) x = sub(x, mul(S.ld[k][col].w, S.bop[r][k].w));
+        }
+        S.b[r][col] = x;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
+    const int rr = e / (int)n, cc = e % (int)n;
+    if (rr < rows) B[(r0 + rr) * ldb + cc] = S.b[rr][cc];
+  }
 }
 
 // ---- Cholesky leaf: b <= 32 diagonal block, one CTA, thread (i, j) owns a_ij --
@@ -576,6 +755,21 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
 int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, const int32_t* stop,
                  cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
+  if (n <= FR_NMAX) {
+    // one fused launch: each CTA solves FR_ROWS whole rows
+    static int w = -1;
+    if (w < 0) {
+      const char* e = getenv("POSIT_RLTN_W");
+      w = e ? atoi(e) : FR_W;
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrSmem<8>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrSmem<16>));
+    }
+    pb_count_launch();
+    const unsigned g = (unsigned)((m + FR_ROWS - 1) / FR_ROWS);
+    if (w == 8) k_trsm_rltn_fused<8><<<g, FR_ROWS * 8, sizeof(FrSmem<8>), st>>>(L, ldl, B, ldb, m, n, stop, 1);
+    else k_trsm_rltn_fused<16><<<g, FR_ROWS * 16, sizeof(FrSmem<16>), st>>>(L, ldl, B, ldb, m, n, stop, 1);
+    return last_launch();
+  }
   for (int64_t j0 = 0; j0 < n; j0 += TBR) {
     const int64_t jb = (n - j0) < TBR ? (n - j0) : TBR;
     pb_count_launch();
