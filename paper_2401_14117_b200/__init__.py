@@ -28,7 +28,7 @@ POSIT_NAR = 0x80000000
 OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libposit_b200.so")
+LIB_PATH = os.environ.get("POSIT_LIB_PATH") or os.path.join(_HERE, "libposit_b200.so")
 _lib = None
 
 

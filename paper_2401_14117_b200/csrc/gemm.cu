@@ -6,7 +6,17 @@
 #include "gemm.cuh"
 #include "internal.h"
 
+#ifndef PG_KK_UNROLL
+#define PG_KK_UNROLL 1
+#endif
+
 namespace pg {
+
+constexpr int KK_UNROLL = PG_KK_UNROLL;   // k-steps of the fast loop unrolled (each TM x TN MACs)
+#ifndef PG_GROUP_M
+#define PG_GROUP_M 32
+#endif
+constexpr int GROUP_M = PG_GROUP_M;       // row tiles per rasterisation group
 
 // Tile configuration.  One CTA = BM x BN outputs, NTHR threads, each thread a
 // TM x TN register tile of decoded accumulators; operands staged in k-slabs
@@ -77,8 +87,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   const int tid = threadIdx.x;
   const int tx = tid % C::NTX;             // column group
   const int ty = tid / C::NTX;             // row group
-  const int64_t row0 = (int64_t)blockIdx.y * BM;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  // grouped rasterisation: consecutive CTAs sweep the column tiles of a group
+  // of GROUP_M row tiles, so a wave re-reads its A rows and B columns from L2
+  const int64_t nbn = gridDim.x, nbm = gridDim.y;
+  const int64_t pid = (int64_t)blockIdx.y * nbn + blockIdx.x;
+  const int64_t per_group = (int64_t)GROUP_M * nbn;
+  const int64_t gfirst = (pid / per_group) * GROUP_M;
+  const int64_t gsize = (nbm - gfirst) < GROUP_M ? (nbm - gfirst) : GROUP_M;
+  const int64_t row0 = (gfirst + (pid % per_group) % gsize) * BM;
+  const int64_t col0 = ((pid % per_group) / gsize) * BN;
   if (SYRK && col0 > row0 + BM - 1) return;   // tile entirely above the diagonal
   if (P.stop != nullptr && *P.stop != 0) return;
 
@@ -180,7 +197,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     const int kmax = (int)min((int64_t)BK, P.k - k0);
     if (!special) {
       if (kmax == BK) {
-#pragma unroll 2
+#pragma unroll (KK_UNROLL)
         for (int kk = 0; kk < BK; kk++) {
           uint4 av[TM], bv[TN];
 #pragma unroll

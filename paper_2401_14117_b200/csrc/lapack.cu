@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <cooperative_groups.h>
 #include "gemm.cuh"
 #include "internal.h"
 
@@ -60,6 +61,8 @@ __device__ __forceinline__ unsigned long long block_max(unsigned long long v, un
 struct LeafWs {
   unsigned long long key[64];
   unsigned int done;
+  uint32_t rowp[64];       // cooperative leaf: the pivot row and the current row, published
+  uint32_t rowj[64];
 };
 
 // key[0] <- max over rows 0..m-1 of column 0
@@ -134,6 +137,86 @@ __global__ void k_leaf_update(uint32_t* A, int64_t lda, int64_t m, int64_t w, in
   }
   best = block_max(best, red);
   if (threadIdx.x == 0 && best != 0ull) atomicMax(&ws->key[j + 1], best);
+}
+
+// ---- LU leaf as ONE cooperative launch ---------------------------------------
+// The leaf (m rows x w <= 64 columns) is split into contiguous row ranges, one
+// per CTA, kept in shared memory for all w steps.  Per column j: every CTA
+// folds its pivot candidates into key[j] (64-bit atomicMax), grid sync; the
+// CTAs owning rows j and p publish them, grid sync; then each CTA swaps,
+// divides and updates its own rows (textbook order, Q8/Q10/Q11) and folds the
+// next column's candidates.  Bit-identical to the per-column launches.
+namespace cg = cooperative_groups;
+constexpr int COOP_THREADS = 256;
+
+__global__ void __launch_bounds__(COOP_THREADS) k_leaf_coop(uint32_t* A, int64_t lda, int64_t m, int64_t w,
+                                                            int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
+                                                            int64_t row_base, LeafWs* ws) {
+  extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
+  __shared__ unsigned long long red[COOP_THREADS / 32];
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t re = (rb + rows_per_cta) < m ? (rb + rows_per_cta) : m;
+  const int nr = re > rb ? (int)(re - rb) : 0;
+  const int W = (int)w;
+  for (int e = tid; e < nr * W; e += COOP_THREADS) tile[e] = A[(rb + e / W) * lda + e % W];
+  __syncthreads();
+  // candidates of column 0
+  {
+    unsigned long long best = 0ull;
+    for (int i = tid; i < nr; i += COOP_THREADS) {
+      const unsigned long long k = piv_key(tile[i * W], rb + i);
+      best = k > best ? k : best;
+    }
+    best = block_max(best, red);
+    if (tid == 0 && best != 0ull) atomicMax(&ws->key[0], best);
+  }
+  const int64_t jmax = m < w ? m : w;
+  for (int64_t j = 0; j < jmax; j++) {
+    grid.sync();
+    const unsigned long long key = *(volatile unsigned long long*)&ws->key[j];
+    const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+    // publish rows p and j
+    if (p >= rb && p < re) for (int c = tid; c < W; c += COOP_THREADS) ws->rowp[c] = tile[(p - rb) * W + c];
+    if (j >= rb && j < re) for (int c = tid; c < W; c += COOP_THREADS) ws->rowj[c] = tile[(j - rb) * W + c];
+    grid.sync();
+    const uint32_t v = ((volatile uint32_t*)ws->rowp)[j];
+    if (blockIdx.x == 0 && tid == 0) {
+      ipiv[j] = (int32_t)(row_base + p + 1);
+      if (v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
+    }
+    if (v != 0u && p != j) {                          // swap rows j and p (whole leaf width)
+      if (j >= rb && j < re) for (int c = tid; c < W; c += COOP_THREADS) tile[(j - rb) * W + c] = ((volatile uint32_t*)ws->rowp)[c];
+      if (p >= rb && p < re) for (int c = tid; c < W; c += COOP_THREADS) tile[(p - rb) * W + c] = ((volatile uint32_t*)ws->rowj)[c];
+    }
+    __syncthreads();
+    // divide column j below the diagonal (Q8; skipped for a zero pivot, Q11)
+    const int64_t i0 = (j + 1 > rb ? j + 1 : rb) - rb;
+    if (v != 0u)
+      for (int64_t i = i0 + tid; i < nr; i += COOP_THREADS) tile[i * W + j] = div(tile[i * W + j], v);
+    __syncthreads();
+    // update columns j+1..w-1 of rows j+1..m-1 with row j (= the pivot row), then fold column j+1
+    const int wq = W - (int)j - 1;
+    unsigned long long best = 0ull;
+    if (wq > 0) {
+      const uint32_t* rowj = (v != 0u && p != j) ? ws->rowp : ws->rowj;   // the row now at position j
+      for (int64_t e = tid; e < (nr - i0) * wq; e += COOP_THREADS) {
+        const int64_t i = i0 + e / wq;
+        const int q = (int)j + 1 + (int)(e % wq);
+        const uint32_t nv = sub(tile[i * W + q], mul(tile[i * W + j], ((volatile const uint32_t*)rowj)[q]));
+        tile[i * W + q] = nv;
+        if (q == j + 1) {
+          const unsigned long long k = piv_key(nv, rb + i);
+          best = k > best ? k : best;
+        }
+      }
+      best = block_max(best, red);
+      if (tid == 0 && best != 0ull) atomicMax(&ws->key[j + 1], best);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * W; e += COOP_THREADS) A[(rb + e / W) * lda + e % W] = tile[e];
 }
 
 // laswp: rows k1..k2-1 swapped with ipiv[k]-1-base, in order, on columns
@@ -679,6 +762,32 @@ static int64_t panel_leaf() {
 static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
                       LeafWs* ws, cudaStream_t st) {
   if (cudaMemsetAsync(ws, 0, sizeof(LeafWs), st) != cudaSuccess) return POSIT_ECUDA;
+  // one cooperative launch when the rows fit the CTAs' shared memory
+  static int coop = -1;
+  static int nsm = 148;
+  if (coop < 0) {
+    const char* e = getenv("POSIT_LEAF_COOP");
+    coop = e ? atoi(e) : 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int ok = 0;
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    if (!ok) coop = 0;
+    cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  }
+  const int64_t rpc = (m + nsm - 1) / nsm;
+  const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
+  if (coop && smem <= 160 * 1024 && w <= 64) {
+    int64_t mm = m, ww = w, rr = rpc, rbase = row_base, ld = lda;
+    void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws};
+    const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
+    pb_count_launch();
+    if (cudaLaunchCooperativeKernel((const void*)k_leaf_coop, dim3(grid), dim3(COOP_THREADS), args, smem, st) ==
+        cudaSuccess)
+      return last_launch();
+    (void)cudaGetLastError();                          // fall back to the per-column launches
+  }
   pb_count_launch();
   k_leaf_colmax<<<rows_grid(m, 256), 256, 0, st>>>(A, lda, m, ws);
   const int64_t jmax = m < w ? m : w;
