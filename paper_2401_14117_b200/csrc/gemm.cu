@@ -196,6 +196,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     if (t + 1 < ntiles) load_tile(k0 + BK);
     const int kmax = (int)min((int64_t)BK, P.k - k0);
     if (!special) {
+      // the accumulators must start the slab within the range that keeps every
+      // MAC of the slab exact (E_ACC_SLAB, see mac); clamp for the table bounds
+#pragma unroll
+      for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+          bad = bad | (acc[i][j].E > E_ACC_SLAB);
+          acc[i][j].E = min(acc[i][j].E, E_CLAMP);
+        }
       if (kmax == BK) {
 #pragma unroll (KK_UNROLL)
         for (int kk = 0; kk < BK; kk++) {
@@ -208,8 +217,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y, (int32_t)bv[j].z,
-                  K, badacc);
+              mac<MacConst, false>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y,
+                                   (int32_t)bv[j].z, K, badacc);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
@@ -222,17 +231,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y, (int32_t)bv[j].z,
-                  K, badacc);
+              mac<MacConst, false>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y,
+                                   (int32_t)bv[j].z, K, badacc);
         }
       }
-      // once per k-slab: fold the accumulated flags, bound the scales (table range)
-      bad = bad | (badacc >= BAD_FLAG);
-      badacc = 0u;
-#pragma unroll
-      for (int i = 0; i < TM; i++)
-#pragma unroll
-        for (int j = 0; j < TN; j++) acc[i][j].E = min(acc[i][j].E, E_CLAMP);
     } else if (!bad) {
       // generic path for this k-slab (a zero / NaR / extreme operand is present)
 #pragma unroll

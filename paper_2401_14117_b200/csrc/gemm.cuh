@@ -31,7 +31,8 @@
 
 namespace pg {
 
-constexpr int E_STAGE_MAX = 53;    // |Ea|,|Eb| <= 53  ->  |Ea+Eb+1| <= 107
+constexpr int E_STAGE_MAX = 37;    // |Ea|,|Eb| <= 37  ->  |Ep| <= 75: the sum never needs |E| > 107 (see mac)
+constexpr int E_ACC_SLAB = 91;     // accumulator |E| <= 91 at a k-slab start: +1 per MAC stays <= 107
 constexpr int T_FAST_MAX = 26;     // f_s >= 1  <=>  t <= 26
 constexpr int E_ZERO = -2048;      // scale used for a zero accumulator
 
@@ -89,7 +90,7 @@ __device__ __forceinline__ bool acc_decode(uint32_t x, Acc& c) {
 // powers of two so that the shifts they drive run as IMAD / IMAD.WIDE on the
 // FMA pipe instead of SHF on the (bottleneck) ALU pipe:
 //   product, indexed by Ep:  { 2^(30-t), -2^(29-t), 2^(t+3), 0 }
-//   sum,     indexed by Ex:  { 2^(27-t) (0 if t > 26), 2^(t+3), BAD_FLAG if t > 26, 0 }
+//   sum,     indexed by Ex:  { 2^(27-t) (0 if t > 26), 2^(t+3), BAD_FLAG if t > 26, Ex }
 constexpr int TBIAS = 192;               // table index = E + TBIAS, E in [-192, 191]
 constexpr int TSIZE = 384;
 constexpr uint32_t BAD_FLAG = 1u << 23;  // accumulated with IMAD; checked once per k-slab
@@ -103,7 +104,7 @@ __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int n
     const bool fast = t <= (uint32_t)T_FAST_MAX;
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;        // keep the product constants finite
     tp[i] = make_uint4(1u << (30 - tc), 0u - (1u << (29 - tc)), 1u << (tc + 3), 0u);
-    tx[i] = make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, 0u);
+    tx[i] = make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
   }
 }
 
@@ -149,15 +150,18 @@ struct CalcConst {
     const uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     const bool fast = t <= (uint32_t)T_FAST_MAX;
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;
-    return make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, 0u);
+    return make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
   }
 };
 
 // ---- the decoded-domain MAC -------------------------------------------------
 // c <- c (+) (a (x) b), a = (Ma hidden@31, Ea, sa), b = (Mb hidden@30, Eb, sb),
-// signs as +1/-1 ints.  badacc accumulates BAD_FLAG when the sum leaves the
-// fast range (the caller checks it once per k-slab).
-template <class Tab>
+// signs as +1/-1 ints.  With TRACK, badacc accumulates BAD_FLAG when the sum
+// leaves the exact range |E| <= 107 (the caller checks it once per k-slab).
+// The GEMM does not track per MAC: with |Ea|, |Eb| <= 37 (staging) and
+// |Ec| <= 91 at the slab start, |Ep| <= 75, a sum's scale grows by at most 1
+// per MAC (<= 107 after 16) and cancellation stops at Ebg - 31 >= -106.
+template <class Tab, bool TRACK = true>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
@@ -211,9 +215,9 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   c.M = Mn >> cy;
   // exact cancellation (x == 0, flo = -1): scale pushed far below any product,
   // so the (zero) accumulator is the small operand of every later add
-  c.E = (int32_t)fmad((uint32_t)((int32_t)flo >> 31), 4096u, fmad(cy, K.one, Exi - 30u));
+  c.E = (int32_t)fmad((uint32_t)((int32_t)flo >> 31), 4096u, U.w + cy);
   c.sg = sbg;
-  badacc = fmad(U.z, K.one, badacc);                          // BAD_FLAG bits accumulate
+  if (TRACK) badacc = fmad(U.z, K.one, badacc);               // BAD_FLAG bits accumulate
 }
 
 // ---- decoded-domain division -----------------------------------------------

@@ -115,3 +115,18 @@ def test_gemm_bad_arguments(cuda_ok):
         PB.posit_gemm(A, A, A, alpha=O.from_f64(2.0))
     with pytest.raises(PB.PositError):
         PB.posit_gemm(A, A, A, beta=O.from_f64(0.5))
+
+
+@pytest.mark.parametrize("ea,ec", [(36, 88), (38, 92), (-36, -100), (-38, 40), (30, 100)])
+def test_gemm_fast_path_range_boundaries(cuda_ok, ea, ec):
+    # operand scales straddling the staging limit (|E| <= 37 -> fast slab) and
+    # accumulator scales straddling the per-slab limit (|E| <= 91), plus growth
+    # within a slab: the fast path, the generic slab and the thread recompute
+    # must all give the oracle's bits
+    rng = np.random.default_rng(abs(ea) * 1000 + abs(ec))
+    m, n, k = 70, 130, 48
+    A = np.ldexp(rng.uniform(1.0, 2.0, (m, k)) * rng.choice([-1.0, 1.0], (m, k)), ea + rng.integers(-2, 3, (m, k)))
+    B = np.ldexp(rng.uniform(1.0, 2.0, (k, n)) * rng.choice([-1.0, 1.0], (k, n)), ea + rng.integers(-2, 3, (k, n)))
+    C = np.ldexp(rng.standard_normal((m, n)), ec + rng.integers(-3, 4, (m, n)))
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
