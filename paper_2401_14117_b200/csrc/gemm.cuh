@@ -31,6 +31,9 @@
 
 namespace pg {
 
+#ifndef PG_PROD_BY_SUM
+#define PG_PROD_BY_SUM 1
+#endif
 constexpr int E_STAGE_MAX = 37;    // |Ea|,|Eb| <= 37  ->  |Ep| <= 75: the sum never needs |E| > 107 (see mac)
 constexpr int E_ACC_SLAB = 91;     // accumulator |E| <= 91 at a k-slab start: +1 per MAC stays <= 107
 constexpr int T_FAST_MAX = 26;     // f_s >= 1  <=>  t <= 26
@@ -103,7 +106,17 @@ __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int n
     uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     const bool fast = t <= (uint32_t)T_FAST_MAX;
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;        // keep the product constants finite
+#if PG_PROD_BY_SUM
+    // indexed by S = Ea + Eb: {2^(30 - t0), 2^(29 - t1) - 2^(30 - t0), 2^(t0 + 3), 2^(t1 + 3) - 2^(t0 + 3)}
+    // with t0 = t(S) (product normalised at n = 0) and t1 = t(S + 1) (n = 1)
+    const int E1 = E + 1;
+    uint32_t t1 = (uint32_t)(E1 ^ (E1 >> 31)) >> 2;
+    t1 = t1 < (uint32_t)T_FAST_MAX ? t1 : (uint32_t)T_FAST_MAX;
+    tp[i] = make_uint4(1u << (30 - tc), (1u << (29 - t1)) - (1u << (30 - tc)), 1u << (tc + 3),
+                       (1u << (t1 + 3)) - (1u << (tc + 3)));
+#else
     tp[i] = make_uint4(1u << (30 - tc), 0u - (1u << (29 - tc)), 1u << (tc + 3), 0u);
+#endif
     tx[i] = make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
   }
 }
@@ -133,6 +146,7 @@ struct MacConst {
   uint32_t one, sixteen;               // = 1, 16 at run time (opaque to ptxas)
   uint32_t tp0, tx0;                   // shared-memory byte addresses of table entry E = 0 (tx: Ex + 30 = 0)
   __device__ __forceinline__ uint4 prod(int32_t Ep) const { return lds128(fmad((uint32_t)Ep, sixteen, tp0)); }
+  __device__ __forceinline__ uint4 prod2(int32_t S) const { return lds128(fmad((uint32_t)S, sixteen, tp0)); }
   __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(fmad(Exi, sixteen, tx0)); }
 };
 
@@ -144,6 +158,15 @@ struct CalcConst {
     uint32_t t = (uint32_t)(Ep ^ (Ep >> 31)) >> 2;
     t = t < (uint32_t)T_FAST_MAX ? t : (uint32_t)T_FAST_MAX;
     return make_uint4(1u << (30 - t), 0u - (1u << (29 - t)), 1u << (t + 3), 0u);
+  }
+  __device__ __forceinline__ uint4 prod2(int32_t S) const {
+    uint32_t t0 = (uint32_t)(S ^ (S >> 31)) >> 2;
+    t0 = t0 < (uint32_t)T_FAST_MAX ? t0 : (uint32_t)T_FAST_MAX;
+    const int32_t S1 = S + 1;
+    uint32_t t1 = (uint32_t)(S1 ^ (S1 >> 31)) >> 2;
+    t1 = t1 < (uint32_t)T_FAST_MAX ? t1 : (uint32_t)T_FAST_MAX;
+    return make_uint4(1u << (30 - t0), (1u << (29 - t1)) - (1u << (30 - t0)), 1u << (t0 + 3),
+                      (1u << (t1 + 3)) - (1u << (t0 + 3)));
   }
   __device__ __forceinline__ uint4 sum(uint32_t Exi) const {
     const int32_t E = (int32_t)Exi - 30;
@@ -168,8 +191,16 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   uint32_t hi, lo;
   mulwide(Ma, Mb, hi, lo);                            // hi in [2^29, 2^31)
   const uint32_t n = hi >> 30;
+#if PG_PROD_BY_SUM
+  // the table lookup depends only on Ea + Eb, so it overlaps the multiply
+  const uint4 T = K.prod2(Ea + Eb);
+  const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
+  const uint32_t mulp = fmad(n, T.w, T.z);
+#else
   const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
   const uint4 T = K.prod(Ep);
+  const uint32_t mulp = T.z;
+#endif
   // drop D = t + 2 + n bits of hi: hi * 2^(32 - D) splits into q (high) and the dropped bits (low, left-aligned)
   uint32_t qp, yp;
   mulwide(hi, fmad(n, T.y, T.x), qp, yp);
@@ -179,7 +210,7 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
       "addc.cc.u32 t, %2, 0x7FFFFFFF;\n\t"            // CF = round up (RNE)
       "addc.u32 %0, %3, 0;\n\t}"
       : "=r"(rp) : "r"(lo), "r"(yp | (qp & 1u)), "r"(qp));
-  const uint32_t Mp = fmad(rp, T.z, 0u);              // hidden@30 (2^31 if rounding carried)
+  const uint32_t Mp = fmad(rp, mulp, 0u);             // hidden@30 (2^31 if rounding carried)
   const int32_t sp = (int32_t)fmad((uint32_t)sa, (uint32_t)sb, 0u);
 
   // -- sum: exact aligned add with jammed sticky, rounded once at f_s(Ex) --
