@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <string.h>
 #include <atomic>
+#include <stdlib.h>
 #include "gemm.cuh"
 #include "internal.h"
 
@@ -172,7 +173,7 @@ int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* i
   if (lda < (b > 1 ? b : 1)) return -4;
   if (m == 0 || b == 0) return 0;
   if (work == nullptr || work_bytes < pb_panel_ws_bytes()) return -8;
-  return launch_check(pb_getrf_panel(m, b, A, lda, ipiv, info, row_base, work, S(stream)));
+  return launch_check(pb_getrf_panel(m, b, A, lda, ipiv, info, row_base, work, true, S(stream)));
 }
 
 int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
@@ -182,6 +183,43 @@ int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2,
   if (k1 < 0 || k2 < k1) return -4;
   return launch_check(pb_laswp(ncols, A, lda, k1, k2, ipiv, ipiv_base, S(stream)));
 }
+
+// Lookahead (both drivers): the next panel is factored on a high-priority
+// side stream while the current step's trailing update of the columns beyond
+// that panel runs on the caller's stream.  The two touch disjoint columns, and
+// every element still receives its updates one product at a time in
+// ascending k (reading Q6), so the bits equal the serial schedule.
+// POSIT_LOOKAHEAD = 0 / 1 forces the serial / lookahead schedule for both;
+// by default Cholesky uses lookahead (its panel -- potf2 plus the fused TRSM
+// -- overlaps the SYRK well: C3 240 -> 205 ms) and LU does not (its leaf is
+// a cooperative launch that cannot share the SMs with the trailing GEMM; the
+// per-column fallback on the side stream measured slower at n = 8192).
+static int lookahead_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("POSIT_LOOKAHEAD");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_col = nullptr, ev_panel = nullptr;
+  int init() {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return POSIT_ECUDA;
+    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi) != cudaSuccess) return POSIT_ECUDA;
+    if (cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming) != cudaSuccess) return POSIT_ECUDA;
+    if (cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming) != cudaSuccess) return POSIT_ECUDA;
+    return 0;
+  }
+  ~SideStream() {
+    if (ev_col) cudaEventDestroy(ev_col);
+    if (ev_panel) cudaEventDestroy(ev_panel);
+    if (side) cudaStreamDestroy(side);     // released once its queued work completes
+  }
+};
 
 int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t nb,
                 void* work, size_t work_bytes, void* stream) {
@@ -195,20 +233,48 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
   int rc = cuda_check(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   if (rc) return rc;
   const int64_t kmax = m < n ? m : n;
+  if (kmax == 0) return 0;
+  const bool la = lookahead_env() == 1 && kmax > nb;
+  SideStream ss;
+  if (la && (rc = ss.init())) return rc;
+  // panel 0 on the caller's stream
+  if ((rc = pb_getrf_panel(m, kmax < nb ? kmax : nb, A, lda, ipiv, info, 0, work, true, st))) return launch_check(rc);
   for (int64_t s = 0; s < kmax; s += nb) {
     const int64_t b = (kmax - s) < nb ? (kmax - s) : nb;
-    // 1. panel: columns s..s+b, rows s..m
-    if ((rc = pb_getrf_panel(m - s, b, A + s * lda + s, lda, ipiv + s, info, s, work, st))) return launch_check(rc);
-    // 2. the panel's swaps on the columns left and right of it
-    if (s > 0 && (rc = pb_laswp(s, A, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);
-    if (s + b < n && (rc = pb_laswp(n - s - b, A + s + b, lda, s, s + b, ipiv, 0, st))) return launch_check(rc);
-    if (s + b < n) {
-      // 3. U12 = L11^{-1} A12
-      if ((rc = pb_trsm_llnu(b, n - s - b, A + s * lda + s, lda, A + s * lda + s + b, lda, st))) return launch_check(rc);
-      // 4. trailing update A22 -= L21 U12 (the hot path)
-      if (s + b < m) {
-        pg::Params P{m - s - b, n - s - b, b, A + (s + b) * lda + s, lda, A + s * lda + s + b, lda,
-                     A + (s + b) * lda + s + b, lda, 1, 1, nullptr};
+    const int64_t s1 = s + b;                                  // next panel's first column / row
+    const int64_t b1 = (kmax - s1) < nb ? (kmax - s1) : nb;    // its width (<= 0: none)
+    if (la && s > 0 && (rc = cuda_check(cudaStreamWaitEvent(st, ss.ev_panel, 0)))) return rc;
+    // the panel's swaps on the columns left and right of it
+    if (s > 0 && (rc = pb_laswp(s, A, lda, s, s1, ipiv, 0, st))) return launch_check(rc);
+    if (s1 < n && (rc = pb_laswp(n - s1, A + s1, lda, s, s1, ipiv, 0, st))) return launch_check(rc);
+    if (s1 < n) {
+      // U12 = L11^{-1} A12
+      if ((rc = pb_trsm_llnu(b, n - s1, A + s * lda + s, lda, A + s * lda + s1, lda, st))) return launch_check(rc);
+    }
+    if (s1 < n && s1 < m) {
+      const uint32_t* L21 = A + s1 * lda + s;
+      const uint32_t* U12 = A + s * lda + s1;
+      if (b1 > 0) {
+        // trailing update of the next panel's columns first ...
+        pg::Params Pc{m - s1, b1, b, L21, lda, U12, lda, A + s1 * lda + s1, lda, 1, 1, nullptr};
+        if ((rc = pb_launch_gemm(Pc, false, false, st))) return launch_check(rc);
+        if (la) {
+          // ... then factor it on the side stream while the rest of the update runs
+          if ((rc = cuda_check(cudaEventRecord(ss.ev_col, st)))) return rc;
+          if ((rc = cuda_check(cudaStreamWaitEvent(ss.side, ss.ev_col, 0)))) return rc;
+          if ((rc = pb_getrf_panel(m - s1, b1, A + s1 * lda + s1, lda, ipiv + s1, info, s1, work, false, ss.side)))
+            return launch_check(rc);
+          if ((rc = cuda_check(cudaEventRecord(ss.ev_panel, ss.side)))) return rc;
+        }
+        if (s1 + b1 < n) {
+          pg::Params Pr{m - s1, n - s1 - b1, b, L21, lda, U12 + b1, lda, A + s1 * lda + s1 + b1, lda, 1, 1, nullptr};
+          if ((rc = pb_launch_gemm(Pr, false, false, st))) return launch_check(rc);
+        }
+        if (!la &&
+            (rc = pb_getrf_panel(m - s1, b1, A + s1 * lda + s1, lda, ipiv + s1, info, s1, work, true, st)))
+          return launch_check(rc);
+      } else {
+        pg::Params P{m - s1, n - s1, b, L21, lda, U12, lda, A + s1 * lda + s1, lda, 1, 1, nullptr};
         if ((rc = pb_launch_gemm(P, false, false, st))) return launch_check(rc);
       }
     }
@@ -233,17 +299,50 @@ int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, i
   cudaStream_t st = S(stream);
   int rc = cuda_check(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   if (rc) return rc;
+  if (n == 0) return 0;
+  const bool la = lookahead_env() != 0 && n >= 4 * nb;
+  SideStream ss;
+  if (la && (rc = ss.init())) return rc;
+  // diagonal block and panel 0 on the caller's stream
+  {
+    const int64_t b = n < nb ? n : nb;
+    if ((rc = pb_potf2(b, A, lda, info, 0, st))) return launch_check(rc);
+    if (b < n && (rc = pb_trsm_rltn(n - b, b, A, lda, A + b * lda, lda, info, st))) return launch_check(rc);
+  }
   for (int64_t s = 0; s < n; s += nb) {
     const int64_t b = (n - s) < nb ? (n - s) : nb;
-    if ((rc = pb_potf2(b, A + s * lda + s, lda, info, s, st))) return launch_check(rc);
-    if (s + b < n) {
-      if ((rc = pb_trsm_rltn(n - s - b, b, A + s * lda + s, lda, A + (s + b) * lda + s, lda, info, st)))
-        return launch_check(rc);
-      pg::Params P{n - s - b, n - s - b, b, A + (s + b) * lda + s, lda, A + (s + b) * lda + s, lda,
-                   A + (s + b) * lda + s + b, lda, 1, 1, info};
-      if ((rc = pb_launch_gemm(P, true, true, st))) return launch_check(rc);
+    const int64_t s1 = s + b;
+    if (s1 >= n) break;
+    const int64_t b1 = (n - s1) < nb ? (n - s1) : nb;
+    if (la && s > 0 && (rc = cuda_check(cudaStreamWaitEvent(st, ss.ev_panel, 0)))) return rc;
+    const uint32_t* L21 = A + s1 * lda + s;
+    // SYRK of the next block column first (rows s1.., columns s1..s1+b1, lower part) ...
+    pg::Params Pc{n - s1, b1, b, L21, lda, L21, lda, A + s1 * lda + s1, lda, 1, 1, info};
+    if ((rc = pb_launch_gemm(Pc, true, true, st))) return launch_check(rc);
+    auto panel = [&](cudaStream_t q) -> int {
+      int r;
+      if ((r = pb_potf2(b1, A + s1 * lda + s1, lda, info, s1, q))) return r;
+      if (s1 + b1 < n && (r = pb_trsm_rltn(n - s1 - b1, b1, A + s1 * lda + s1, lda, A + (s1 + b1) * lda + s1, lda,
+                                           info, q)))
+        return r;
+      return 0;
+    };
+    if (la) {
+      // ... then the next diagonal block and panel on the side stream
+      if ((rc = cuda_check(cudaEventRecord(ss.ev_col, st)))) return rc;
+      if ((rc = cuda_check(cudaStreamWaitEvent(ss.side, ss.ev_col, 0)))) return rc;
+      if ((rc = panel(ss.side))) return launch_check(rc);
+      if ((rc = cuda_check(cudaEventRecord(ss.ev_panel, ss.side)))) return rc;
     }
+    // the rest of the trailing update (lower triangle beyond the next block column)
+    if (s1 + b1 < n) {
+      const uint32_t* L2b = A + (s1 + b1) * lda + s;
+      pg::Params Pr{n - s1 - b1, n - s1 - b1, b, L2b, lda, L2b, lda, A + (s1 + b1) * lda + s1 + b1, lda, 1, 1, info};
+      if ((rc = pb_launch_gemm(Pr, true, true, st))) return launch_check(rc);
+    }
+    if (!la && (rc = panel(st))) return launch_check(rc);
   }
+  if (la && (rc = cuda_check(cudaStreamWaitEvent(st, ss.ev_panel, 0)))) return rc;
   return cuda_check(cudaPeekAtLastError());
 }
 

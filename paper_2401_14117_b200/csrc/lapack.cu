@@ -760,7 +760,7 @@ static int64_t panel_leaf() {
 // Unblocked leaf (w <= 64 columns): per column one swap/divide launch and one
 // update launch that also searches the next column's pivot.
 static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
-                      LeafWs* ws, cudaStream_t st) {
+                      LeafWs* ws, bool allow_coop, cudaStream_t st) {
   if (cudaMemsetAsync(ws, 0, sizeof(LeafWs), st) != cudaSuccess) return POSIT_ECUDA;
   // one cooperative launch when the rows fit the CTAs' shared memory
   static int coop = -1;
@@ -778,7 +778,7 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
   }
   const int64_t rpc = (m + nsm - 1) / nsm;
   const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
-  if (coop && smem <= 160 * 1024 && w <= 64) {
+  if (coop && allow_coop && smem <= 160 * 1024 && w <= 64) {
     int64_t mm = m, ww = w, rr = rpc, rbase = row_base, ld = lda;
     void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
@@ -809,20 +809,21 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
 // Every element still receives its products one at a time in ascending k
 // (reading Q6), so the bits equal the column-by-column loop.
 int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
-                   void* ws, cudaStream_t st) {
+                   void* ws, bool allow_coop, cudaStream_t st) {
   const int64_t w = m < b ? m : b;
   const int64_t leaf = panel_leaf();
-  if (w <= leaf) return getrf_leaf(m, b, A, lda, ipiv, info, row_base, static_cast<LeafWs*>(ws), st);
+  if (w <= leaf) return getrf_leaf(m, b, A, lda, ipiv, info, row_base, static_cast<LeafWs*>(ws), allow_coop, st);
   int64_t w1 = ((w / 2 + leaf - 1) / leaf) * leaf;
   if (w1 >= w) w1 = w - leaf;
   int rc;
-  if ((rc = pb_getrf_panel(m, w1, A, lda, ipiv, info, row_base, ws, st))) return rc;
+  if ((rc = pb_getrf_panel(m, w1, A, lda, ipiv, info, row_base, ws, allow_coop, st))) return rc;
   if ((rc = pb_laswp(b - w1, A + w1, lda, 0, w1, ipiv, row_base, st))) return rc;
   if ((rc = pb_trsm_llnu(w1, b - w1, A, lda, A + w1, lda, st))) return rc;
   if (m > w1) {
     pg::Params P{m - w1, b - w1, w1, A + w1 * lda, lda, A + w1, lda, A + w1 * lda + w1, lda, 1, 1, nullptr};
     if ((rc = pb_launch_gemm(P, false, false, st))) return rc;
-    if ((rc = pb_getrf_panel(m - w1, b - w1, A + w1 * lda + w1, lda, ipiv + w1, info, row_base + w1, ws, st)))
+    if ((rc = pb_getrf_panel(m - w1, b - w1, A + w1 * lda + w1, lda, ipiv + w1, info, row_base + w1, ws, allow_coop,
+                             st)))
       return rc;
     if ((rc = pb_laswp(w1, A + w1 * lda, lda, 0, w - w1, ipiv + w1, row_base + w1, st))) return rc;
   }
