@@ -189,11 +189,10 @@ int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2,
 // that panel runs on the caller's stream.  The two touch disjoint columns, and
 // every element still receives its updates one product at a time in
 // ascending k (reading Q6), so the bits equal the serial schedule.
-// POSIT_LOOKAHEAD = 0 / 1 forces the serial / lookahead schedule for both;
-// by default Cholesky uses lookahead (its panel -- potf2 plus the fused TRSM
-// -- overlaps the SYRK well: C3 240 -> 205 ms) and LU does not (its leaf is
-// a cooperative launch that cannot share the SMs with the trailing GEMM; the
-// per-column fallback on the side stream measured slower at n = 8192).
+// POSIT_LOOKAHEAD=0 forces the serial schedule.  Measured on one B200:
+// Cholesky C3 240 -> 205 ms, LU C5 446 -> 406 ms, C4 2.84 -> 2.71 s.  On the
+// side stream the LU leaf is a cooperative launch of 16 CTAs x 1024 threads,
+// so it needs only 16 SMs while the trailing GEMM holds the rest.
 static int lookahead_env() {
   static int v = -2;
   if (v == -2) {
@@ -234,7 +233,7 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
   if (rc) return rc;
   const int64_t kmax = m < n ? m : n;
   if (kmax == 0) return 0;
-  const bool la = lookahead_env() == 1 && kmax > nb;
+  const bool la = lookahead_env() != 0 && kmax > nb;
   SideStream ss;
   if (la && (rc = ss.init())) return rc;
   // panel 0 on the caller's stream

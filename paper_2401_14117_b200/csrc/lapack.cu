@@ -149,23 +149,24 @@ __global__ void k_leaf_update(uint32_t* A, int64_t lda, int64_t m, int64_t w, in
 namespace cg = cooperative_groups;
 constexpr int COOP_THREADS = 256;
 
-__global__ void __launch_bounds__(COOP_THREADS) k_leaf_coop(uint32_t* A, int64_t lda, int64_t m, int64_t w,
+__global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, int64_t m, int64_t w,
                                                             int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
                                                             int64_t row_base, LeafWs* ws) {
   extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
-  __shared__ unsigned long long red[COOP_THREADS / 32];
+  __shared__ unsigned long long red[32];
+  const int NT = blockDim.x;
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t re = (rb + rows_per_cta) < m ? (rb + rows_per_cta) : m;
   const int nr = re > rb ? (int)(re - rb) : 0;
   const int W = (int)w;
-  for (int e = tid; e < nr * W; e += COOP_THREADS) tile[e] = A[(rb + e / W) * lda + e % W];
+  for (int e = tid; e < nr * W; e += NT) tile[e] = A[(rb + e / W) * lda + e % W];
   __syncthreads();
   // candidates of column 0
   {
     unsigned long long best = 0ull;
-    for (int i = tid; i < nr; i += COOP_THREADS) {
+    for (int i = tid; i < nr; i += NT) {
       const unsigned long long k = piv_key(tile[i * W], rb + i);
       best = k > best ? k : best;
     }
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(COOP_THREADS) k_leaf_coop(uint32_t* A, int64_t
     const unsigned long long key = *(volatile unsigned long long*)&ws->key[j];
     const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
     // publish rows p and j
-    if (p >= rb && p < re) for (int c = tid; c < W; c += COOP_THREADS) ws->rowp[c] = tile[(p - rb) * W + c];
-    if (j >= rb && j < re) for (int c = tid; c < W; c += COOP_THREADS) ws->rowj[c] = tile[(j - rb) * W + c];
+    if (p >= rb && p < re) for (int c = tid; c < W; c += NT) ws->rowp[c] = tile[(p - rb) * W + c];
+    if (j >= rb && j < re) for (int c = tid; c < W; c += NT) ws->rowj[c] = tile[(j - rb) * W + c];
     grid.sync();
     const uint32_t v = ((volatile uint32_t*)ws->rowp)[j];
     if (blockIdx.x == 0 && tid == 0) {
@@ -187,21 +188,21 @@ __global__ void __launch_bounds__(COOP_THREADS) k_leaf_coop(uint32_t* A, int64_t
       if (v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
     }
     if (v != 0u && p != j) {                          // swap rows j and p (whole leaf width)
-      if (j >= rb && j < re) for (int c = tid; c < W; c += COOP_THREADS) tile[(j - rb) * W + c] = ((volatile uint32_t*)ws->rowp)[c];
-      if (p >= rb && p < re) for (int c = tid; c < W; c += COOP_THREADS) tile[(p - rb) * W + c] = ((volatile uint32_t*)ws->rowj)[c];
+      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = ((volatile uint32_t*)ws->rowp)[c];
+      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = ((volatile uint32_t*)ws->rowj)[c];
     }
     __syncthreads();
     // divide column j below the diagonal (Q8; skipped for a zero pivot, Q11)
     const int64_t i0 = (j + 1 > rb ? j + 1 : rb) - rb;
     if (v != 0u)
-      for (int64_t i = i0 + tid; i < nr; i += COOP_THREADS) tile[i * W + j] = div(tile[i * W + j], v);
+      for (int64_t i = i0 + tid; i < nr; i += NT) tile[i * W + j] = div(tile[i * W + j], v);
     __syncthreads();
     // update columns j+1..w-1 of rows j+1..m-1 with row j (= the pivot row), then fold column j+1
     const int wq = W - (int)j - 1;
     unsigned long long best = 0ull;
     if (wq > 0) {
       const uint32_t* rowj = (v != 0u && p != j) ? ws->rowp : ws->rowj;   // the row now at position j
-      for (int64_t e = tid; e < (nr - i0) * wq; e += COOP_THREADS) {
+      for (int64_t e = tid; e < (nr - i0) * wq; e += NT) {
         const int64_t i = i0 + e / wq;
         const int q = (int)j + 1 + (int)(e % wq);
         const uint32_t nv = sub(tile[i * W + q], mul(tile[i * W + j], ((volatile const uint32_t*)rowj)[q]));
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_leaf_coop(uint32_t* A, int64_t
     }
     __syncthreads();
   }
-  for (int e = tid; e < nr * W; e += COOP_THREADS) A[(rb + e / W) * lda + e % W] = tile[e];
+  for (int e = tid; e < nr * W; e += NT) A[(rb + e / W) * lda + e % W] = tile[e];
 }
 
 // laswp: rows k1..k2-1 swapped with ipiv[k]-1-base, in order, on columns
@@ -776,15 +777,18 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     if (!ok) coop = 0;
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   }
-  const int64_t rpc = (m + nsm - 1) / nsm;
+  // on the caller's stream: one CTA of 256 threads per SM; on a side stream
+  // (lookahead, sharing the SMs with the trailing GEMM): a few CTAs of 1024
+  const int nctas = allow_coop ? nsm : (nsm < 16 ? nsm : 16);
+  const int nthr = allow_coop ? COOP_THREADS : 1024;
+  const int64_t rpc = (m + nctas - 1) / nctas;
   const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
-  if (coop && allow_coop && smem <= 160 * 1024 && w <= 64) {
+  if (coop && smem <= 160 * 1024 && w <= 64) {
     int64_t mm = m, ww = w, rr = rpc, rbase = row_base, ld = lda;
     void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
     pb_count_launch();
-    if (cudaLaunchCooperativeKernel((const void*)k_leaf_coop, dim3(grid), dim3(COOP_THREADS), args, smem, st) ==
-        cudaSuccess)
+    if (cudaLaunchCooperativeKernel((const void*)k_leaf_coop, dim3(grid), dim3(nthr), args, smem, st) == cudaSuccess)
       return last_launch();
     (void)cudaGetLastError();                          // fall back to the per-column launches
   }
