@@ -351,7 +351,7 @@ def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):
     peak = N_SM * LANES_PER_SM * f_max / 1e12
     achieved = macs * inst_per_mac / t / 1e12
     return {"bound": "alu", "unit": "Tinst/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
-            "traffic": prof.get("dram_bytes_per_launch"), "kernel": "pg::k_gemm<false,false>",
+            "traffic": prof.get("dram_bytes_per_launch"), "kernel": prof.get("kernel", "pg::k_gemm (NN)"),
             "kernel_ms": t * 1e3, "inst_per_mac": inst_per_mac, "inst_per_mac_source": src,
             "peak_source": f"148 SMs x 4 SMSP x 32 lanes x sm_max_mhz {f_max / 1e6:.0f} (MEASURED_PEAKS.json) "
                            "= warp-instruction issue limit; see DESIGN.md",
