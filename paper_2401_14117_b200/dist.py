@@ -18,6 +18,8 @@ Per panel step s (columns [s nb, s nb + b)), owner o = s mod P:
   3. every rank: laswp of the step's b interchanges on all its other columns,
      U12 = L11^-1 A12 (unit-lower TRSM) and A22 <- A22 - L21 U12 (the hot GEMM)
      on its columns right of the panel.
+With lookahead the owner of panel s+1 updates and factors it before the rest
+of step s's update, and its broadcast overlaps that update (side stream).
 No reductions in the data path.  By the order contract (Q6) every
 element still receives its products one at a time in ascending k, so the
 factors are bit-identical to the single-GPU posit_getrf and to the textbook
@@ -118,61 +120,153 @@ class CudaOps:
 
 
 def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, info: torch.Tensor,
-               ops=None, group=None) -> None:
+               ops=None, group=None, lookahead: bool = True) -> None:
     """In-place distributed LU with partial pivoting of the n x n matrix whose
     local columns (desc.scatter) are A_local (int32 pattern storage, row-major).
 
     ipiv (int32, n) receives the global 1-based pivots on EVERY rank; info
     (int32, 1) the first zero-pivot column (1-based) or 0, on every rank.
+
+    Lookahead (CUDA tensors): the owner of panel s+1 updates that panel's
+    columns first, factors it and starts its broadcast on a high-priority side
+    stream, while every rank's trailing update of step s continues on the
+    current stream; the broadcast is awaited only when step s+1 is applied.
     """
-    steps = getrf_dist_steps(A_local, desc, ipiv, info, CudaOps() if ops is None else ops)
-    for s, buf in enumerate(steps):
-        if desc.nprocs > 1:
-            dist.broadcast(buf, src=desc.owner(s), group=group)
+    ops = CudaOps() if ops is None else ops
+    cuda = A_local.is_cuda and lookahead
+    P = desc.nprocs
+    if not cuda:
+        steps = getrf_dist_steps(A_local, desc, ipiv, info, ops)
+        for s, buf in steps:
+            if P > 1:
+                dist.broadcast(buf, src=desc.owner(s), group=group)
+        return
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream(device=A_local.device, priority=-1)
+    pending = {}
+
+    class _OnSide:
+        def __enter__(self):
+            side.wait_stream(main)
+            self._ctx = torch.cuda.stream(side)
+            self._ctx.__enter__()
+
+        def __exit__(self, *a):
+            return self._ctx.__exit__(*a)
+
+    def on_use(s):
+        main.wait_stream(side)
+        w = pending.pop(s, None)
+        if w is not None:
+            w.wait()
+
+    steps = getrf_dist_steps(A_local, desc, ipiv, info, ops, panel_ctx=_OnSide, on_use=on_use)
+    for s, buf in steps:
+        buf.record_stream(side)              # allocated on the main stream, used on the side stream too
+        if P > 1:
+            with torch.cuda.stream(side):
+                side.wait_stream(main)
+                pending[s] = dist.broadcast(buf, src=desc.owner(s), group=group, async_op=True)
+    main.wait_stream(side)
 
 
-def getrf_dist_steps(A_local, desc: BlockCyclic1D, ipiv, info, ops):
-    """The per-rank schedule of getrf_dist as a generator: for each panel step
-    s it runs the panel phase, yields the packed [panel | ipiv | info] buffer
-    (filled on the owner), expects it to hold the owner's data when resumed
-    (the broadcast), and then runs the swap / TRSM / trailing-GEMM phase."""
-    n, nb, P, me = desc.n, desc.nb, desc.nprocs, desc.rank
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def getrf_dist_steps(A_local, desc: BlockCyclic1D, ipiv, info, ops, panel_ctx=None, on_use=None):
+    """The per-rank schedule of getrf_dist as a generator, in lookahead order.
+
+    It yields (s, buf) once per panel s: buf is the packed
+    [panel | ipiv | info] buffer of panel s, filled on the owner; the caller
+    broadcasts it (possibly asynchronously).  on_use(s) is called right before
+    buf is first read on this rank.  panel_ctx() wraps the owner's work on the
+    next panel (its factorisation and packing), e.g. to run it on a side stream.
+    Step s: apply panel s (laswp, U12 TRSM); the owner of panel s+1 updates its
+    columns of that block, factors and packs it -> yield; then every rank
+    updates its remaining trailing columns with step s."""
+    panel_ctx = panel_ctx or _Null
+    on_use = on_use or (lambda s: None)
+    n, nb, me = desc.n, desc.nb, desc.rank
     if A_local.shape != (n, desc.local_cols()):
         raise ValueError(f"A_local has shape {tuple(A_local.shape)}, expected {(n, desc.local_cols())}")
     dev = A_local.device
     info.zero_()
     my_info = torch.zeros(1, dtype=torch.int32, device=dev)
     nloc = A_local.shape[1]
-    for s in range(desc.nblocks):
-        r0 = s * nb
+    nblk = desc.nblocks
+
+    def new_buf(s):
+        m = n - s * nb
         b = desc.block_width(s)
+        return torch.empty(m * b + b + 1, dtype=torch.int32, device=dev)
+
+    def factor_and_pack(s, buf):
+        r0, b = s * nb, desc.block_width(s)
+        m = n - r0
+        lc = desc.local_offset(s)
+        Ap = A_local[r0:, lc: lc + b]
+        ops.getrf_panel(Ap, ipiv[r0: r0 + b], my_info, r0)
+        buf[: m * b].view(m, b).copy_(Ap)
+        buf[m * b: m * b + b].copy_(ipiv[r0: r0 + b])
+        buf[m * b + b: m * b + b + 1].copy_(my_info)
+
+    buf = new_buf(0)
+    if me == desc.owner(0):
+        with panel_ctx():
+            factor_and_pack(0, buf)
+    yield 0, buf
+    for s in range(nblk):
+        r0, b = s * nb, desc.block_width(s)
         m = n - r0
         o = desc.owner(s)
-        buf = torch.empty(m * b + b + 1, dtype=torch.int32, device=dev)
+        on_use(s)
         panel = buf[: m * b].view(m, b)
-        if me == o:
-            lc = desc.local_offset(s)
-            Ap = A_local[r0:, lc: lc + b]
-            ops.getrf_panel(Ap, ipiv[r0: r0 + b], my_info, r0)
-            panel.copy_(Ap)
-            buf[m * b: m * b + b].copy_(ipiv[r0: r0 + b])
-            buf[m * b + b: m * b + b + 1].copy_(my_info)
-        yield buf
         if me != o:
             ipiv[r0: r0 + b].copy_(buf[m * b: m * b + b])
         # first zero pivot so far, identical on every rank (the owner's counter is cumulative)
         step_info = buf[m * b + b: m * b + b + 1]
         info.copy_(torch.where(info != 0, info, step_info))
-        # 3. interchanges on every local column outside this panel
+        # interchanges on every local column outside this panel
         if me == o:
             lc = desc.local_offset(s)
             ops.laswp(A_local[:, :lc], r0, r0 + b, ipiv)
             ops.laswp(A_local[:, lc + b:], r0, r0 + b, ipiv)
         else:
             ops.laswp(A_local, r0, r0 + b, ipiv)
-        # 4. U12 and the trailing update on the columns right of the panel
+        # U12 on the columns right of the panel
         t0 = desc.first_local_after(s)
-        if t0 < nloc and r0 + b <= n:
+        if t0 < nloc:
             ops.trsm_llnu(panel[:b], A_local[r0: r0 + b, t0:])
-            if r0 + b < n:
-                ops.gemm_minus(panel[b:], A_local[r0: r0 + b, t0:], A_local[r0 + b:, t0:])
+        L21 = panel[b:]
+        r1 = r0 + b
+        if s + 1 < nblk:
+            o1 = desc.owner(s + 1)
+            nxt = new_buf(s + 1)
+            if me == o1:
+                # the next panel's columns first, then factor it (side stream under lookahead)
+                lc1 = desc.local_offset(s + 1)
+                b1 = desc.block_width(s + 1)
+                if r1 < n:
+                    ops.gemm_minus(L21, A_local[r0: r1, lc1: lc1 + b1], A_local[r1:, lc1: lc1 + b1])
+                with panel_ctx():
+                    factor_and_pack(s + 1, nxt)
+            yield s + 1, nxt
+            # the rest of step s's trailing update
+            if t0 < nloc and r1 < n:
+                if me == o1:
+                    lc1 = desc.local_offset(s + 1)
+                    b1 = desc.block_width(s + 1)
+                    if t0 < lc1:
+                        ops.gemm_minus(L21, A_local[r0: r1, t0: lc1], A_local[r1:, t0: lc1])
+                    if lc1 + b1 < nloc:
+                        ops.gemm_minus(L21, A_local[r0: r1, lc1 + b1:], A_local[r1:, lc1 + b1:])
+                else:
+                    ops.gemm_minus(L21, A_local[r0: r1, t0:], A_local[r1:, t0:])
+            buf = nxt
+        elif t0 < nloc and r1 < n:
+            ops.gemm_minus(L21, A_local[r0: r1, t0:], A_local[r1:, t0:])

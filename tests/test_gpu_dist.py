@@ -39,15 +39,16 @@ def test_getrf_dist_emulated_ranks_cuda(cuda_ok, P):
     ipivs = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(P)]
     infos = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(P)]
     steps = [D.getrf_dist_steps(locs[r], descs[r], ipivs[r], infos[r], CudaOps()) for r in range(P)]
-    # each generator yields its step-s broadcast buffer after the panel phase;
-    # the 'broadcast' is a device copy from the owner's buffer, then all resume
-    bufs = [next(g) for g in steps]
+    # each generator yields (s, buffer of panel s) at its broadcast point (lookahead
+    # order); the 'broadcast' is a device copy from the owner's buffer, then all resume
+    items = [next(g) for g in steps]
     for s in range(descs[0].nblocks):
+        assert all(it[0] == s for it in items)
         for r in range(P):
             if r != s % P:
-                bufs[r].copy_(bufs[s % P])
-        bufs = [next(g, None) for g in steps]
-    assert all(b is None for b in bufs)
+                items[r][1].copy_(items[s % P][1])
+        items = [next(g, None) for g in steps]
+    assert all(it is None for it in items)
     full_out = descs[0].gather([t.cpu() for t in locs]).numpy().view(np.uint32)
     ref, rpiv, rinfo = O.getrf(A)
     assert mismatch(full_out, ref) == 0
