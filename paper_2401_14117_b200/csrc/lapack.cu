@@ -437,9 +437,9 @@ __global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64
 // GEMM's shared-memory constant tables; L's block column staged decoded,
 // k-major so a lane group reads consecutive words).  Per element the updates
 // still arrive one at a time in ascending k (Q6).
-constexpr int FR_ROWS = 32, FR_NMAX = 256, FR_W = 16;
+constexpr int FR_NMAX = 256, FR_W = 16;
 
-template <int W>
+template <int W, int FR_ROWS>
 struct FrSmem {
   uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
   uint4 ld[W][FR_NMAX];                       // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
@@ -454,13 +454,13 @@ struct FrSmem {
   uint4 tx[pg::TSIZE];
 };
 
-template <int W>
+template <int W, int FR_ROWS>
 __global__ void __launch_bounds__(FR_ROWS * W) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
                                                                  int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
                                                                  int one) {
   constexpr int NT = FR_ROWS * W;
   extern __shared__ __align__(16) unsigned char fr_raw[];
-  FrSmem<W>& S = *reinterpret_cast<FrSmem<W>*>(fr_raw);
+  FrSmem<W, FR_ROWS>& S = *reinterpret_cast<FrSmem<W, FR_ROWS>*>(fr_raw);
   if (stop != nullptr && *stop != 0) return;
   const int tid = threadIdx.x;
   const int r = tid / W, c = tid % W;                  // row of the tile, column within a block
@@ -871,17 +871,22 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   if (m <= 0 || n <= 0) return 0;
   if (n <= FR_NMAX) {
     // one fused launch: each CTA solves FR_ROWS whole rows
-    static int w = -1;
-    if (w < 0) {
-      const char* e = getenv("POSIT_RLTN_W");
-      w = e ? atoi(e) : FR_W;
-      cudaFuncSetAttribute(k_trsm_rltn_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrSmem<8>));
-      cudaFuncSetAttribute(k_trsm_rltn_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrSmem<16>));
+    static int rows = -1;
+    if (rows < 0) {
+      const char* e = getenv("POSIT_RLTN_ROWS");
+      rows = e ? atoi(e) : 16;
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 16>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 32>));
     }
     pb_count_launch();
-    const unsigned g = (unsigned)((m + FR_ROWS - 1) / FR_ROWS);
-    if (w == 8) k_trsm_rltn_fused<8><<<g, FR_ROWS * 8, sizeof(FrSmem<8>), st>>>(L, ldl, B, ldb, m, n, stop, 1);
-    else k_trsm_rltn_fused<16><<<g, FR_ROWS * 16, sizeof(FrSmem<16>), st>>>(L, ldl, B, ldb, m, n, stop, 1);
+    if (rows == 32)
+      k_trsm_rltn_fused<16, 32><<<(unsigned)((m + 31) / 32), 32 * 16, sizeof(FrSmem<16, 32>), st>>>(L, ldl, B, ldb, m,
+                                                                                                   n, stop, 1);
+    else
+      k_trsm_rltn_fused<16, 16><<<(unsigned)((m + 15) / 16), 16 * 16, sizeof(FrSmem<16, 16>), st>>>(L, ldl, B, ldb, m,
+                                                                                                   n, stop, 1);
     return last_launch();
   }
   for (int64_t j0 = 0; j0 < n; j0 += TBR) {
