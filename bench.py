@@ -88,10 +88,12 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": float(np.median(pw)) if pw else None}
 
 
 def _load_json(path):
@@ -284,6 +286,13 @@ def run_ours(args):
                 "clocks": clk.summary(), "gpu_launches": launches,
                 "paper_context": {"gemm_gflops_rtx4090_n8000": 181.4, "gemm_gflops_agilex_n8000": 202.7,
                                   "lu_gflops_rx7900_n8000": 13.4, "source": "PAPER.md:403,432,542"}}
+
+    # ---- energy efficiency (Table PowerE analog): NVML board power of
+    # this GPU during the timed region, not the paper's AC wall power
+    if rank == 0:
+        pw = line["clocks"].get("power_w_median")
+        line["efficiency"] = {"board_power_w": pw, "gflops_per_w": (value / world / pw) if pw else None,
+                              "paper": "LU 0.076 Gflops/W RX7900 + host, AC wall (P:591)"}
 
     # ---- roofline of the dominant kernel (GEMM), timed alone on this stream --
     if args.workload == "gemm" and rank == 0:
