@@ -180,7 +180,8 @@ def _config(args):
                 "n": 16384, "nb": 256, "l2": "matrix 1 GiB > L2",
                 "parallelism": (f"1x{args.gpus} column-block-cyclic, NCCL panel broadcast" if args.gpus > 1 else "single GPU")}
     return {"workload": "configs[2]: Posit(32,2) Cholesky, n=8192, nb=256, A = G G^T/n + I seed 2",
-            "n": 8192, "nb": 256, "l2": "matrix 256 MiB > L2", "parallelism": f"replica x{args.gpus}"}
+            "n": 8192, "nb": 256, "l2": "matrix 256 MiB > L2",
+            "parallelism": (f"1x{args.gpus} column-block-cyclic, NCCL panel broadcast" if args.gpus > 1 else "single GPU")}
 
 
 # ---------------------------------------------------------------------- our arm
@@ -241,17 +242,30 @@ def run_ours(args):
                 PB.posit_getrf(dA, ipiv, info, nb=SI.C4_NB)
     else:
         nn = SI.C3_N
-        dA0 = PB.posit_from_f64(torch.from_numpy(SI.config3()).to(dev))
-        dA = dA0.clone()
+        full = PB.posit_from_f64(torch.from_numpy(SI.config3()).to(dev))
         info = torch.zeros(1, dtype=torch.int32, device=dev)
         flops = nn ** 3 / 3.0
+        if world > 1:
+            # configs[2]: ONE n = 8192 Cholesky shared by all ranks (1 x P column-block-cyclic)
+            from paper_2401_14117_b200.dist import BlockCyclic1D, potrf_dist
+            desc = BlockCyclic1D(nn, SI.C3_NB, world, rank)
+            dA0 = desc.scatter(full)
+            del full
+            dA = dA0.clone()
 
-        def step():
-            dA.copy_(dA0)
-            PB.posit_potrf(dA, info, nb=SI.C3_NB)
-    # whole-job work: GEMM and Cholesky run one problem per rank (weak scaling);
-    # the LU is one problem distributed over all ranks (strong scaling)
-    strong = args.workload == "lu" and world > 1
+            def step():
+                dA.copy_(dA0)
+                potrf_dist(dA, desc, info)
+        else:
+            dA0 = full
+            dA = dA0.clone()
+
+            def step():
+                dA.copy_(dA0)
+                PB.posit_potrf(dA, info, nb=SI.C3_NB)
+    # whole-job work: the GEMM runs one problem per rank (weak scaling); LU and
+    # Cholesky are one problem distributed over all ranks (strong scaling)
+    strong = args.workload in ("lu", "cholesky") and world > 1
     job_flops = flops if strong else world * flops
 
     for _ in range(args.warmup):

@@ -270,3 +270,146 @@ def getrf_dist_steps(A_local, desc: BlockCyclic1D, ipiv, info, ops, panel_ctx=No
             buf = nxt
         elif t0 < nloc and r1 < n:
             ops.gemm_minus(L21, A_local[r0: r1, t0:], A_local[r1:, t0:])
+
+
+# ---------------------------------------------------------------- Cholesky ----
+# the same 1 x P column-block-cyclic layout for the lower
+# Cholesky factorisation.  Per step s the owner factors the diagonal block
+# (potf2) and solves the rows below it (L21 = A21 L11^-T), packs the panel and
+# its info flag, and broadcasts; every rank then applies the symmetric update
+# to its own later column blocks: for block j > s, rows >= j nb,
+#     A[r, c] <- A[r, c] (-) L[r, s-block] . L[c, s-block]^T   (c <= r),
+# as a SYRK on the diagonal block and an NT GEMM below it.  Same lookahead as
+# the LU.  No pivoting, no reductions; bits identical for every P (Q6).
+
+class CudaCholOps:
+    """The Cholesky arithmetic through the C ABI (current CUDA stream)."""
+
+    def __init__(self):
+        import paper_2401_14117_b200 as PB
+        self.PB = PB
+
+    def potrf_block(self, D, info, row_base):
+        """Factor the b x b diagonal block D (lower); a failure sets info = row_base + k + 1."""
+        loc = torch.zeros(1, dtype=torch.int32, device=D.device)
+        self.PB.posit_potrf(D, loc, nb=max(D.shape[0], 1))
+        info.copy_(torch.where((info == 0) & (loc != 0), loc + row_base, info))
+
+    def trsm_rltn(self, L, B):
+        if B.shape[0] > 0:
+            self.PB.posit_trsm("R", "L", "T", "N", L, B)
+
+    def syrk_minus(self, A, C):
+        if C.shape[0] > 0:
+            self.PB.posit_syrk(A, C)
+
+    def gemm_nt_minus(self, A, B, C):
+        if C.shape[0] > 0 and C.shape[1] > 0:
+            self.PB.posit_gemm(A, B, C, transb="T")
+
+
+def potrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, info: torch.Tensor, ops=None, group=None,
+               lookahead: bool = True) -> None:
+    """In-place distributed lower Cholesky of the n x n SPD matrix whose local
+    column blocks (desc.scatter) are A_local.  info (int32, 1) receives the
+    first failing column (1-based) or 0 on every rank; after a failure only
+    info and the blocks before the failing one are defined (as posit_potrf)."""
+    ops = CudaCholOps() if ops is None else ops
+    cuda = A_local.is_cuda and lookahead
+    P = desc.nprocs
+    if not cuda:
+        for s, buf in potrf_dist_steps(A_local, desc, info, ops):
+            if P > 1:
+                dist.broadcast(buf, src=desc.owner(s), group=group)
+        return
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream(device=A_local.device, priority=-1)
+    pending = {}
+
+    class _OnSide:
+        def __enter__(self):
+            side.wait_stream(main)
+            self._ctx = torch.cuda.stream(side)
+            self._ctx.__enter__()
+
+        def __exit__(self, *a):
+            return self._ctx.__exit__(*a)
+
+    def on_use(s):
+        main.wait_stream(side)
+        w = pending.pop(s, None)
+        if w is not None:
+            w.wait()
+
+    for s, buf in potrf_dist_steps(A_local, desc, info, ops, panel_ctx=_OnSide, on_use=on_use):
+        buf.record_stream(side)
+        if P > 1:
+            with torch.cuda.stream(side):
+                side.wait_stream(main)
+                pending[s] = dist.broadcast(buf, src=desc.owner(s), group=group, async_op=True)
+    main.wait_stream(side)
+
+
+def potrf_dist_steps(A_local, desc: BlockCyclic1D, info, ops, panel_ctx=None, on_use=None):
+    """The per-rank Cholesky schedule as a generator (lookahead order); yields
+    (s, buf) with buf = [panel (n - s nb) x b | info] filled on the owner."""
+    panel_ctx = panel_ctx or _Null
+    on_use = on_use or (lambda s: None)
+    n, nb, me = desc.n, desc.nb, desc.rank
+    if A_local.shape != (n, desc.local_cols()):
+        raise ValueError(f"A_local has shape {tuple(A_local.shape)}, expected {(n, desc.local_cols())}")
+    dev = A_local.device
+    info.zero_()
+    my_info = torch.zeros(1, dtype=torch.int32, device=dev)
+    nblk = desc.nblocks
+
+    def new_buf(s):
+        m = n - s * nb
+        b = desc.block_width(s)
+        return torch.empty(m * b + 1, dtype=torch.int32, device=dev)
+
+    def factor_and_pack(s, buf):
+        r0, b = s * nb, desc.block_width(s)
+        m = n - r0
+        lc = desc.local_offset(s)
+        D = A_local[r0: r0 + b, lc: lc + b]
+        ops.potrf_block(D, my_info, r0)
+        ops.trsm_rltn(D, A_local[r0 + b:, lc: lc + b])
+        buf[: m * b].view(m, b).copy_(A_local[r0:, lc: lc + b])
+        buf[m * b: m * b + 1].copy_(my_info)
+
+    def update_block(s, panel, j):
+        """Block j (> s) of this rank: rows >= j nb get the step-s update."""
+        r0, rj, bj = s * nb, j * nb, desc.block_width(j)
+        lcj = desc.local_offset(j)
+        Lrows = panel[rj - r0:]                        # L[r, s-block] for r >= j nb
+        Lj = panel[rj - r0: rj - r0 + bj]              # L[c, s-block] for c in block j
+        ops.syrk_minus(Lj, A_local[rj: rj + bj, lcj: lcj + bj])
+        if rj + bj < n:
+            ops.gemm_nt_minus(Lrows[bj:], Lj, A_local[rj + bj:, lcj: lcj + bj])
+
+    buf = new_buf(0)
+    if me == desc.owner(0):
+        with panel_ctx():
+            factor_and_pack(0, buf)
+    yield 0, buf
+    for s in range(nblk):
+        r0, b = s * nb, desc.block_width(s)
+        m = n - r0
+        on_use(s)
+        panel = buf[: m * b].view(m, b)
+        step_info = buf[m * b: m * b + 1]
+        info.copy_(torch.where(info != 0, info, step_info))
+        mine = [j for j in desc.local_blocks() if j > s]
+        if s + 1 < nblk:
+            o1 = desc.owner(s + 1)
+            nxt = new_buf(s + 1)
+            if me == o1:
+                update_block(s, panel, s + 1)
+                with panel_ctx():
+                    factor_and_pack(s + 1, nxt)
+            yield s + 1, nxt
+            for j in mine:
+                if j != s + 1:
+                    update_block(s, panel, j)
+            buf = nxt

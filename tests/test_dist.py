@@ -115,3 +115,58 @@ def test_getrf_dist_gloo_zero_pivot_info():
     ref, rpiv, rinfo = O.getrf(A)
     assert rinfo == 21
     assert int(np.count_nonzero(full != ref)) == 0 and all(i == rinfo for i in infos)
+
+
+# ------------------------------------------------------------- Cholesky ------
+from paper_2401_14117_b200.dist import potrf_dist  # noqa: E402
+
+
+class OracleCholOps:
+    """CPU stand-in for CudaCholOps (tests only)."""
+
+    def potrf_block(self, D, info, row_base):
+        l, inf = O.potrf_lower(_np(D))
+        D.copy_(torch.from_numpy(l.view(np.int32)))
+        if int(info[0]) == 0 and inf != 0:
+            info[0] = inf + row_base
+
+    def trsm_rltn(self, L, B):
+        if B.shape[0]:
+            B.copy_(torch.from_numpy(O.trsm_rltn(_np(L), _np(B)).view(np.int32)))
+
+    def syrk_minus(self, A, C):
+        if C.shape[0]:
+            C.copy_(torch.from_numpy(O.syrk_lower(_np(A), _np(C)).view(np.int32)))
+
+    def gemm_nt_minus(self, A, B, C):
+        if C.shape[0] and C.shape[1]:
+            C.copy_(torch.from_numpy(O.gemm(_np(A), _np(B), _np(C), transb="T").view(np.int32)))
+
+
+def _chol_worker(rank, world, port, A, nb, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = A.shape[0]
+        desc = BlockCyclic1D(n, nb, world, rank)
+        loc = desc.scatter(torch.from_numpy(A.view(np.int32)))
+        info = torch.zeros(1, dtype=torch.int32)
+        potrf_dist(loc, desc, info, ops=OracleCholOps())
+        out[rank] = (loc.numpy().copy(), int(info[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,nb", [(2, 72, 16), (3, 61, 8)])
+def test_potrf_dist_gloo_matches_oracle(world, n, nb):
+    A = O.from_f64_array(SI.config3(n))           # configs[2] recipe (G G^T / n + I) at small n
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_chol_worker, args=(world, _free_port(), A, nb, out), nprocs=world, join=True)
+    desc = BlockCyclic1D(n, nb, world, 0)
+    full = desc.gather([torch.from_numpy(out[r][0]) for r in range(world)]).numpy().view(np.uint32)
+    ref, rinfo = O.potrf_lower(A)
+    il = np.tril_indices(n)
+    assert rinfo == 0 and int(np.count_nonzero(full[il] != ref[il])) == 0
+    assert all(out[r][1] == 0 for r in range(world))

@@ -54,3 +54,40 @@ def test_getrf_dist_emulated_ranks_cuda(cuda_ok, P):
     assert mismatch(full_out, ref) == 0
     for r in range(P):
         assert np.array_equal(ipivs[r].cpu().numpy(), rpiv) and int(infos[r].cpu()[0]) == rinfo
+
+
+def test_potrf_dist_p1_cuda(cuda_ok):
+    from paper_2401_14117_b200.dist import potrf_dist
+    n, nb = 280, 32
+    A = O.from_f64_array(SI.config3(n))
+    desc = BlockCyclic1D(n, nb, 1, 0)
+    loc = desc.scatter(to_dev(A))
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    potrf_dist(loc, desc, info)
+    ref, rinfo = O.potrf_lower(A)
+    il = np.tril_indices(n)
+    assert int(info.cpu()[0]) == rinfo == 0 and mismatch(to_host(loc)[il], ref[il]) == 0
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_potrf_dist_emulated_ranks_cuda(cuda_ok, P):
+    import paper_2401_14117_b200.dist as D
+    n, nb = 190, 16
+    A = O.from_f64_array(SI.config3(n))
+    full = to_dev(A)
+    descs = [BlockCyclic1D(n, nb, P, r) for r in range(P)]
+    locs = [d.scatter(full) for d in descs]
+    infos = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(P)]
+    steps = [D.potrf_dist_steps(locs[r], descs[r], infos[r], D.CudaCholOps()) for r in range(P)]
+    items = [next(g) for g in steps]
+    for s in range(descs[0].nblocks):
+        assert all(it[0] == s for it in items)
+        for r in range(P):
+            if r != s % P:
+                items[r][1].copy_(items[s % P][1])
+        items = [next(g, None) for g in steps]
+    assert all(it is None for it in items)
+    got = descs[0].gather([t.cpu() for t in locs]).numpy().view(np.uint32)
+    ref, rinfo = O.potrf_lower(A)
+    il = np.tril_indices(n)
+    assert mismatch(got[il], ref[il]) == 0 and all(int(i.cpu()[0]) == rinfo for i in infos)
