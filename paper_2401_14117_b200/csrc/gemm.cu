@@ -77,6 +77,20 @@ __device__ __noinline__ uint32_t slow_chain(const uint32_t* A, int64_t lda, cons
   return c;
 }
 
+// Four consecutive words of a row, the ones at index >= avail (or all if
+// !row_ok) replaced by 1.0 (a harmless operand for padded tile slots): one
+// 128-bit read-only load when the quad is complete and 16-byte aligned.
+__device__ __forceinline__ void load_quad(const uint32_t* p, bool row_ok, int64_t avail, uint32_t* out) {
+  if (row_ok && avail >= 4 && (((uintptr_t)p) & 15u) == 0u) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++) out[q] = (row_ok && q < avail) ? __ldg(p + q) : p32::ONE;
+  }
+}
+
 template <class C, bool TRANS_B, bool SYRK>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, TM = C::TM, TN = C::TN, NTHR = C::NTHR;
@@ -130,11 +144,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       const int e = tid + h * NTHR;                   // (row, k quad)
       if (e >= C::AQN) break;
       const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const int64_t r = row0 + ar, kk = k0 + ak + q;
-        ra[h * 4 + q] = (r < P.m && kk < P.k) ? __ldg(P.A + r * P.lda + kk) : p32::ONE;
-      }
+      const int64_t r = row0 + ar, kq = k0 + ak;
+      load_quad(P.A + r * P.lda + kq, r < P.m, P.k - kq, &ra[h * 4]);
     }
 #pragma unroll
     for (int h = 0; h < BQ; h++) {
@@ -142,18 +153,12 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (e >= C::BQN) break;
       if (!TRANS_B) {                                 // (k row, col quad)
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int64_t kk = k0 + bk, cc = col0 + bc + q;
-          rb[h * 4 + q] = (kk < P.k && cc < P.n) ? __ldg(P.B + kk * P.ldb + cc) : p32::ONE;
-        }
+        const int64_t kk = k0 + bk, cq = col0 + bc;
+        load_quad(P.B + kk * P.ldb + cq, kk < P.k, P.n - cq, &rb[h * 4]);
       } else {                                        // (col, k quad)
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int64_t kk = k0 + bk + q, cc = col0 + bc;
-          rb[h * 4 + q] = (kk < P.k && cc < P.n) ? __ldg(P.B + cc * P.ldb + kk) : p32::ONE;
-        }
+        const int64_t kq = k0 + bk, cc = col0 + bc;
+        load_quad(P.B + cc * P.ldb + kq, cc < P.n, P.k - kq, &rb[h * 4]);
       }
     }
   };

@@ -135,9 +135,18 @@ __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& hi, ui
 }
 
 
+#ifndef PG_LDS_VOLATILE
+#define PG_LDS_VOLATILE 0
+#endif
+// Table reads: the tables are written once before the first barrier and never
+// change, so the loads need not be volatile (lets ptxas schedule them freely).
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
+#if PG_LDS_VOLATILE
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+#else
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+#endif
   return v;
 }
 
