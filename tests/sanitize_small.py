@@ -3,7 +3,7 @@ synccheck): GEMM NN/NT/SYRK, LU (recursive panel, cooperative leaf,
 lookahead), Cholesky (potf2 leaf, fused TRSM, lookahead), TRSMs, laswp,
 getrs/potrs, conversions.  Exits 0 if every result matches the oracle.
 
-    compute-sanitizer --tool racecheck python tools/sanitize_small.py
+    compute-sanitizer --tool racecheck python tests/sanitize_small.py
 """
 import os
 import sys
