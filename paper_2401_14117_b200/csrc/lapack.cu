@@ -455,7 +455,7 @@ struct FrSmem {
 };
 
 template <int W, int FR_ROWS>
-__global__ void __launch_bounds__(FR_ROWS * W) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
+__global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
                                                                  int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
                                                                  int one) {
   constexpr int NT = FR_ROWS * W;
@@ -564,24 +564,47 @@ __global__ void __launch_bounds__(FR_ROWS * W) k_trsm_rltn_fused(const uint32_t*
     // A column whose k-loop has only fast operands and an accumulator within
     // |E| <= 75 stays inside the MAC's exact range for all jb <= 16 steps
     // (|Ep| <= 75, |E| grows by <= 1 per step, cancellation stops at >= -106).
+    // Four of the thread's columns are advanced together (independent chains
+    // for ILP); a group with any slow column runs the generic path.
     if (r < rows) {
       const bool rf = S.rowfast[r] != 0;
-      for (int col = c0 + jb + c; col < (int)n; col += W) {
-        uint32_t x = S.b[r][col];
-        pg::Acc a;
-        const bool ok = pg::acc_decode(x, a) && (x == 0u || (a.E <= 75 && a.E >= -75));
-        if (rf && ok && S.colfast[col] != 0) {
-          uint32_t bad = 0u;
-#pragma unroll 4
-          for (int k = 0; k < jb; k++) {
-            const uint4 ad = S.ld[k][col], bd = S.bop[r][k];
-            pg::mac(a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x, (int32_t)bd.y, (int32_t)bd.z, K, bad);
-          }
-          x = pg::acc_encode(a);
-        } else {
-          for (int k = 0; k < jb; k++) x = sub(x, mul(S.ld[k][col].w, S.bop[r][k].w));
+      constexpr int G = 4;
+      for (int col0 = c0 + jb + c; col0 < (int)n; col0 += G * W) {
+        pg::Acc a[G];
+        uint32_t x[G];
+        bool ok = rf;
+#pragma unroll
+        for (int u = 0; u < G; u++) {
+          const int col = col0 + u * W;
+          const bool in = col < (int)n;
+          x[u] = in ? S.b[r][col] : 0u;
+          const bool d = pg::acc_decode(x[u], a[u]) && (x[u] == 0u || (a[u].E <= 75 && a[u].E >= -75));
+          ok = ok && d && (!in || S.colfast[col] != 0);
         }
-        S.b[r][col] = x;
+        if (ok) {
+          uint32_t bad = 0u;
+#pragma unroll 2
+          for (int k = 0; k < jb; k++) {
+            const uint4 bd = S.bop[r][k];
+#pragma unroll
+            for (int u = 0; u < G; u++) {
+              const uint4 ad = S.ld[k][min(col0 + u * W, (int)n - 1)];
+              pg::mac(a[u], ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x, (int32_t)bd.y, (int32_t)bd.z, K, bad);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < G; u++)
+            if (col0 + u * W < (int)n) S.b[r][col0 + u * W] = pg::acc_encode(a[u]);
+        } else {
+#pragma unroll 1
+          for (int u = 0; u < G; u++) {
+            const int col = col0 + u * W;
+            if (col >= (int)n) break;
+            uint32_t y = x[u];
+            for (int k = 0; k < jb; k++) y = sub(y, mul(S.ld[k][col].w, S.bop[r][k].w));
+            S.b[r][col] = y;
+          }
+        }
       }
     }
   }
