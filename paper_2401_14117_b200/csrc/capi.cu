@@ -194,11 +194,10 @@ int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2,
 // side stream the LU leaf is a cooperative launch of 16 CTAs x 1024 threads,
 // so it needs only 16 SMs while the trailing GEMM holds the rest.
 static int lookahead_env() {
-  static int v = -2;
-  if (v == -2) {
+  static const int v = [] {                      // thread-safe one-time init
     const char* e = getenv("POSIT_LOOKAHEAD");
-    v = e ? atoi(e) : -1;
-  }
+    return e ? atoi(e) : -1;
+  }();
   return v;
 }
 

@@ -307,25 +307,26 @@ int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   const dim3 grid((unsigned)((P.n + C::BN - 1) / C::BN), (unsigned)((P.m + C::BM - 1) / C::BM));
   if (grid.y > 65535u) return PB_ERR_TOO_LARGE;
   const size_t smem = sizeof(typename C::Smem);
-  static bool attr_done[4] = {false, false, false, false};
   auto kern = transb ? (syrk ? pg::k_gemm<C, true, true> : pg::k_gemm<C, true, false>)
                      : (syrk ? pg::k_gemm<C, false, true> : pg::k_gemm<C, false, false>);
-  const int idx = (transb ? 2 : 0) + (syrk ? 1 : 0);
-  if (!attr_done[idx]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done[idx] = true;
-  }
+  static const bool attrs = [smem] {           // thread-safe one-time init, all four instantiations
+    cudaFuncSetAttribute(pg::k_gemm<C, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pg::k_gemm<C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pg::k_gemm<C, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pg::k_gemm<C, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return true;
+  }();
+  (void)attrs;
   pb_count_launch();
   kern<<<grid, C::NTHR, smem, st>>>(P);
   return 0;
 }
 
 int variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("POSIT_GEMM_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return v;
 }
 

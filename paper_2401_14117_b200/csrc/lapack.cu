@@ -771,13 +771,11 @@ static int last_launch() {
 size_t pb_panel_ws_bytes() { return sizeof(LeafWs); }
 
 static int64_t panel_leaf() {
-  static int64_t leaf = -1;
-  if (leaf < 0) {
+  static const int64_t leaf = [] {
     const char* e = getenv("POSIT_PANEL_LEAF");
-    leaf = e ? atoll(e) : 32;
-    if (leaf < 1) leaf = 1;
-    if (leaf > 64) leaf = 64;
-  }
+    int64_t v = e ? atoll(e) : 32;
+    return v < 1 ? (int64_t)1 : (v > 64 ? (int64_t)64 : v);
+  }();
   return leaf;
 }
 
@@ -787,19 +785,20 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
                       LeafWs* ws, bool allow_coop, cudaStream_t st) {
   if (cudaMemsetAsync(ws, 0, sizeof(LeafWs), st) != cudaSuccess) return POSIT_ECUDA;
   // one cooperative launch when the rows fit the CTAs' shared memory
-  static int coop = -1;
-  static int nsm = 148;
-  if (coop < 0) {
+  struct CoopCfg { int coop; int nsm; };
+  static const CoopCfg cfg = [] {
+    CoopCfg c{1, 148};
     const char* e = getenv("POSIT_LEAF_COOP");
-    coop = e ? atoi(e) : 1;
-    int dev = 0;
+    c.coop = e ? atoi(e) : 1;
+    int dev = 0, ok = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int ok = 0;
+    cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
-    if (!ok) coop = 0;
+    if (!ok) c.coop = 0;
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-  }
+    return c;
+  }();
+  const int coop = cfg.coop, nsm = cfg.nsm;
   // on the caller's stream: one CTA of 256 threads per SM; on a side stream
   // (lookahead, sharing the SMs with the trailing GEMM): a few CTAs of 1024
   const int nctas = allow_coop ? nsm : (nsm < 16 ? nsm : 16);
@@ -861,11 +860,10 @@ int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, co
              cudaStream_t st) {
   if (ncols <= 0 || k2 <= k1) return 0;
   constexpr size_t smem = 2 * SWP_MAX * SWP_COLS * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_laswp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static const bool attr = [] {
+    return cudaFuncSetAttribute(k_laswp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  }();
+  (void)attr;
   pb_count_launch();
   k_laswp<<<(unsigned)((ncols + SWP_COLS - 1) / SWP_COLS), 256, smem, st>>>(A, lda, ncols, k1, k2, ipiv, ipiv_base);
   return last_launch();
@@ -894,15 +892,14 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   if (m <= 0 || n <= 0) return 0;
   if (n <= FR_NMAX) {
     // one fused launch: each CTA solves FR_ROWS whole rows
-    static int rows = -1;
-    if (rows < 0) {
+    static const int rows = [] {
       const char* e = getenv("POSIT_RLTN_ROWS");
-      rows = e ? atoi(e) : 16;
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 32>));
-    }
+      return e ? atoi(e) : 16;
+    }();
     pb_count_launch();
     if (rows == 32)
       k_trsm_rltn_fused<16, 32><<<(unsigned)((m + 31) / 32), 32 * 16, sizeof(FrSmem<16, 32>), st>>>(L, ldl, B, ldb, m,
@@ -950,12 +947,12 @@ int pb_solve(bool chol, int64_t n, const uint32_t* A, int64_t lda, const int32_t
   if (n <= 0) return 0;
   const size_t smem = (size_t)n * sizeof(uint32_t);
   if (smem > 200 * 1024) return POSIT_ENOTSUP;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {
     cudaFuncSetAttribute(k_getrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_potrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   pb_count_launch();
   if (chol) k_potrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, b);
   else k_getrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, ipiv, b);
