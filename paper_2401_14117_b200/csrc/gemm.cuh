@@ -31,6 +31,9 @@
 
 namespace pg {
 
+#ifndef PG_AD_SAD
+#define PG_AD_SAD 0
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -231,7 +234,11 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   const uint32_t Msm = Mp + c.M - Mbg;                // the other one
   const int32_t sbg = pbig ? sp : c.sg;
   const int32_t Ebg = max(Ep, c.E);
+#if PG_AD_SAD
+  const uint32_t ad = __sad(Ep, c.E, 0u);                      // |Ep - Ec| in one ALU op (FMA pipe is the busier)
+#else
   const uint32_t ad = fmad((uint32_t)Ebg, 2u * K.one, 0u - fmad((uint32_t)Ep, K.one, (uint32_t)c.E));  // |Ep - Ec|
+#endif
   const uint32_t sh = __funnelshift_rc(Msm, 0u, ad);          // Msm >> min(ad, 32)
   const uint32_t lost = __funnelshift_rc(0u, Msm, ad);        // bits shifted out (nonzero iff any)
   uint32_t jam;
