@@ -7,7 +7,9 @@ For each matrix A (binary64): x_sol = 1/sqrt(N), b = A x_sol in
 binary64.  Posit: A and b rounded once to Posit(32,2) (posit_from_f64),
 posit_getrf/potrf + posit_getrs/potrs on the GPU, x back to binary64 exactly.
 binary32: A and b rounded to float32, LAPACK sgetrf/sgetrs or spotrf/spotrs
-(scipy).  binary64: LAPACK dgesv, for the forward error (reading Q18).
+(scipy); and (n <= 2048) binary32 with the posit path's own algorithm and
+operation order (numpy float32 textbook loops, no FMA), so that difference
+isolates the number format.  binary64: LAPACK dgesv, for the forward error (reading Q18).
   e_X      = |b - A x_X| / |b|                         (Eq.4, 2-norm, binary64)
   digits   = log10(e_binary32 / e_posit)               (Eq.5; > 0: posit better)
   fwd_X    = -log10(|x_X - x_64| / |x_64|)             (forward-error digits)
@@ -39,7 +41,52 @@ def _fwd(x, x64):
     return float(-np.log10(max(np.linalg.norm(x - x64) / np.linalg.norm(x64), 1e-300)))
 
 
-def study(name, A, kind, nb=256):
+def _lu32_same_order(A, b):
+    """binary32 with the posit path's operation order: textbook
+    right-looking kij LU with partial pivoting (ties -> smallest row), one division per
+    multiplier, every product and difference rounded to binary32 (numpy float32, no FMA);
+    solves in the Q21 order (forward ascending k, back descending k)."""
+    A = A.astype(np.float32).copy()
+    b = b.astype(np.float32).copy()
+    n = A.shape[0]
+    piv = np.arange(n)
+    for k in range(n):
+        p = k + int(np.argmax(np.abs(A[k:, k])))
+        if p != k:
+            A[[k, p]] = A[[p, k]]
+            piv[[k, p]] = piv[[p, k]]
+        if A[k, k] != 0:
+            A[k + 1:, k] = A[k + 1:, k] / A[k, k]
+        A[k + 1:, k + 1:] = A[k + 1:, k + 1:] - np.outer(A[k + 1:, k], A[k, k + 1:]).astype(np.float32)
+    y = b[piv]
+    for k in range(n):                                   # forward, column-oriented (ascending k)
+        y[k + 1:] = y[k + 1:] - (A[k + 1:, k] * y[k]).astype(np.float32)
+    for k in range(n - 1, -1, -1):                       # back, column-oriented (descending k)
+        y[k] = y[k] / A[k, k]
+        y[:k] = y[:k] - (A[:k, k] * y[k]).astype(np.float32)
+    return y.astype(np.float64)
+
+
+def _chol32_same_order(A, b):
+    A = A.astype(np.float32).copy()
+    y = b.astype(np.float32).copy()
+    n = A.shape[0]
+    for k in range(n):
+        if A[k, k] <= 0:
+            return np.full(n, np.nan)
+        A[k, k] = np.sqrt(A[k, k])
+        A[k + 1:, k] = A[k + 1:, k] / A[k, k]
+        A[k + 1:, k + 1:] = A[k + 1:, k + 1:] - np.outer(A[k + 1:, k], A[k + 1:, k]).astype(np.float32)
+    for k in range(n):
+        y[k] = y[k] / A[k, k]
+        y[k + 1:] = y[k + 1:] - (A[k + 1:, k] * y[k]).astype(np.float32)
+    for k in range(n - 1, -1, -1):
+        y[k] = y[k] / A[k, k]
+        y[:k] = y[:k] - (A[k, :k] * y[k]).astype(np.float32)
+    return y.astype(np.float64)
+
+
+def study(name, A, kind, nb=256, same_order_max=2048):
     n = A.shape[0]
     x_sol = np.full(n, 1.0 / np.sqrt(n))
     b = A @ x_sol
@@ -64,9 +111,16 @@ def study(name, A, kind, nb=256):
     x64 = np.linalg.solve(A, b)
     ep, e32 = _err(A, b, xp), _err(A, b, x32.astype(np.float64))
     ok = ep > 0 and np.isfinite(ep) and np.isfinite(e32)
-    return {"case": name, "kind": kind, "n": n, "info": int(info.cpu()[0]), "e_posit": ep, "e_binary32": e32,
-            "digits_eq5": float(np.log10(e32 / ep)) if ok else None,
-            "fwd_digits_posit": _fwd(xp, x64), "fwd_digits_binary32": _fwd(x32.astype(np.float64), x64)}
+    r = {"case": name, "kind": kind, "n": n, "info": int(info.cpu()[0]), "e_posit": ep, "e_binary32": e32,
+         "digits_eq5": float(np.log10(e32 / ep)) if ok else None,
+         "fwd_digits_posit": _fwd(xp, x64), "fwd_digits_binary32": _fwd(x32.astype(np.float64), x64)}
+    if n <= same_order_max:
+        # the same algorithm and operation order in binary32: isolates the number format
+        xs = _lu32_same_order(A, b) if kind == "lu" else _chol32_same_order(A, b)
+        es = _err(A, b, xs)
+        r["e_binary32_same_order"] = es
+        r["digits_vs_same_order"] = float(np.log10(es / ep)) if (ep > 0 and np.isfinite(es)) else None
+    return r
 
 
 def main():
