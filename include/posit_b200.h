@@ -75,8 +75,9 @@ const char* posit_last_error(void);
  * LU, the hot path.
  *   alpha  must be POSIT_ONE or POSIT_MONE (else -6); beta must be 0 or
  *          POSIT_ONE (else -11) (reading Q7).
- *   transa must be 'N' (transa = 'T' -> POSIT_ENOTSUP); transb 'N' or 'T'.
- *   lda >= k, ldb >= n ('N') or >= k ('T'), ldc >= n.
+ *   transa, transb 'N' or 'T' (the paper's four transpose variants):
+ *   A is stored m x k ('N') or k x m ('T'), B k x n ('N') or n x k ('T').
+ *   lda >= k ('N') or >= m ('T'), ldb >= n ('N') or >= k ('T'), ldc >= n.
  * C must not overlap A or B.
  */
 int posit_gemm(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,

@@ -105,29 +105,30 @@ def _ld(t) -> int:
 
 def posit_gemm(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None,
                transa: str = "N") -> None:
-    """C <- alpha*A*op(B) + beta*C in place (row-major int32 pattern tensors; views with row stride allowed)."""
-    m, k = A.shape
-    n = C.shape[1]
+    """C <- alpha*op(A)*op(B) + beta*C in place (row-major int32 pattern tensors; views with row stride allowed)."""
+    m, n = C.shape
+    k = A.shape[1] if transa == "N" else A.shape[0]
     _check(lib().posit_gemm(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
                             _ptr(C), _ld(C), _stream(stream)), "posit_gemm")
 
 
-def posit_gemm_naive(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None) -> None:
-    m, k = A.shape
-    n = C.shape[1]
-    _check(lib().posit_gemm_naive(b"N", transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
+def posit_gemm_naive(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None,
+                     transa: str = "N") -> None:
+    m, n = C.shape
+    k = A.shape[1] if transa == "N" else A.shape[0]
+    _check(lib().posit_gemm_naive(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
                                   _ptr(C), _ld(C), _stream(stream)), "posit_gemm_naive")
 
 
 def posit_gemm_host(A, B, C, dwork, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE,
-                    stream=None) -> None:
+                    stream=None, transa: str = "N") -> None:
     """HOST-buffer GEMM: A, B, C are CPU (pinned) int32 tensors; dwork a CUDA byte workspace."""
-    m, k = A.shape
-    n = C.shape[1]
+    m, n = C.shape
+    k = A.shape[1] if transa == "N" else A.shape[0]
     for t in (A, B, C):
         if t.is_cuda or not t.is_contiguous():
             raise PositError("posit_gemm_host expects contiguous host tensors")
-    _check(lib().posit_gemm_host(b"N", transb.encode(), m, n, k, alpha, A.data_ptr(), _ld(A), B.data_ptr(), _ld(B),
+    _check(lib().posit_gemm_host(transa.encode(), transb.encode(), m, n, k, alpha, A.data_ptr(), _ld(A), B.data_ptr(), _ld(B),
                                  beta, C.data_ptr(), _ld(C), _ptr(dwork), dwork.numel() * dwork.element_size(),
                                  _stream(stream)), "posit_gemm_host")
 

@@ -54,14 +54,15 @@ static int gemm_common(char transa, char transb, int64_t m, int64_t n, int64_t k
   if (n < 0) return -4;
   if (k < 0) return -5;
   if (alpha != POSIT_ONE && alpha != POSIT_MONE) return -6;
-  if (transa == 'T') return POSIT_ENOTSUP;
-  if (lda < (k > 1 ? k : 1)) return -8;
+  const int64_t acols = transa == 'N' ? k : m;       // A is m x k ('N') or k x m ('T'), row-major
+  if (lda < (acols > 1 ? acols : 1)) return -8;
   if (ldb < ((transb == 'N' ? n : k) > 1 ? (transb == 'N' ? n : k) : 1)) return -10;
   if (beta != 0u && beta != POSIT_ONE) return -11;
   if (ldc < (n > 1 ? n : 1)) return -13;
   if (m == 0 || n == 0) return 0;
   if ((k > 0 && (A == nullptr || B == nullptr)) || C == nullptr) return -7;
   pg::Params P{m, n, k, A, lda, B, ldb, C, ldc, alpha == POSIT_MONE ? 1 : 0, beta == POSIT_ONE ? 1 : 0, nullptr};
+  P.transa = transa == 'T' ? 1 : 0;
   const int rc = naive ? pb_launch_gemm_naive(P, transb == 'T', false, S(stream))
                        : pb_launch_gemm(P, transb == 'T', false, S(stream));
   if (rc) return launch_check(rc);
@@ -87,19 +88,20 @@ size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k) {
 int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
                     int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
                     void* dwork, size_t work_bytes, void* stream) {
-  if (transa != 'N') return transa == 'T' ? POSIT_ENOTSUP : -1;
+  if (transa != 'N' && transa != 'T') return -1;
   if (transb != 'N' && transb != 'T') return -2;
   if (m < 0) return -3;
   if (n < 0) return -4;
   if (k < 0) return -5;
   if (work_bytes < posit_gemm_host_work_bytes(m, n, k) || dwork == nullptr) return -15;
   const int64_t brow = transb == 'N' ? k : n, bcol = transb == 'N' ? n : k;
+  const int64_t arow = transa == 'N' ? m : k, acol = transa == 'N' ? k : m;
   uint32_t* dA = reinterpret_cast<uint32_t*>(dwork);
   uint32_t* dB = dA + m * k;
   uint32_t* dC = dB + k * n;
   cudaStream_t st = S(stream);
   int rc;
-  if ((rc = cuda_check(cudaMemcpy2DAsync(dA, (size_t)k * 4, A, (size_t)lda * 4, (size_t)k * 4, (size_t)m,
+  if ((rc = cuda_check(cudaMemcpy2DAsync(dA, (size_t)acol * 4, A, (size_t)lda * 4, (size_t)acol * 4, (size_t)arow,
                                          cudaMemcpyHostToDevice, st))))
     return rc;
   if ((rc = cuda_check(cudaMemcpy2DAsync(dB, (size_t)bcol * 4, B, (size_t)ldb * 4, (size_t)bcol * 4, (size_t)brow,
@@ -110,7 +112,7 @@ int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, u
                                            cudaMemcpyHostToDevice, st))))
       return rc;
   }
-  rc = posit_gemm(transa, transb, m, n, k, alpha, dA, k > 0 ? k : 1, dB, bcol > 0 ? bcol : 1, beta, dC,
+  rc = posit_gemm(transa, transb, m, n, k, alpha, dA, acol > 0 ? acol : 1, dB, bcol > 0 ? bcol : 1, beta, dC,
                   n > 0 ? n : 1, stream);
   if (rc) return rc;
   if ((rc = cuda_check(cudaMemcpy2DAsync(C, (size_t)ldc * 4, dC, (size_t)n * 4, (size_t)n * 4, (size_t)m,

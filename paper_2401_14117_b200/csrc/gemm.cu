@@ -50,12 +50,12 @@ __device__ __forceinline__ uint32_t mac_generic(uint32_t c, uint32_t a, uint32_t
 // in the fast accumulator.
 __device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, int32_t sg, const uint32_t* A, int64_t lda,
                                         const uint32_t* B, int64_t ldb, int neg, int64_t r, int64_t cc, int64_t k0,
-                                        int kmax, int transb) {
+                                        int kmax, int transb, int transa) {
   Acc acc{M, E, sg};
   uint32_t c = acc_encode(acc);
   for (int kk = 0; kk < kmax; kk++) {
     const int64_t l = k0 + kk;
-    const uint32_t a = A[r * lda + l];
+    const uint32_t a = transa ? A[l * lda + r] : A[r * lda + l];
     const uint32_t b = transb ? B[cc * ldb + l] : B[l * ldb + cc];
     c = mac_generic(c, a, b, neg);
   }
@@ -67,10 +67,10 @@ __device__ __noinline__ uint4 slow_slab(uint32_t M, int32_t E, int32_t sg, const
 // whose fast accumulator left the fast range).
 __device__ __noinline__ uint32_t slow_chain(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb,
                                             const uint32_t* C, int64_t ldc, int beta, int neg, int64_t K, int64_t r,
-                                            int64_t cc, int transb) {
+                                            int64_t cc, int transb, int transa) {
   uint32_t c = beta ? C[r * ldc + cc] : 0u;
   for (int64_t l = 0; l < K; l++) {
-    const uint32_t a = A[r * lda + l];
+    const uint32_t a = transa ? A[l * lda + r] : A[r * lda + l];
     const uint32_t b = transb ? B[cc * ldb + l] : B[l * ldb + cc];
     c = mac_generic(c, a, b, neg);
   }
@@ -143,9 +143,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     for (int h = 0; h < AQ; h++) {
       const int e = tid + h * NTHR;                   // (row, k quad)
       if (e >= C::AQN) break;
-      const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
-      const int64_t r = row0 + ar, kq = k0 + ak;
-      load_quad(P.A + r * P.lda + kq, r < P.m, P.k - kq, &ra[h * 4]);
+      if (!P.transa) {                                // (row, k quad)
+        const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
+        const int64_t r = row0 + ar, kq = k0 + ak;
+        load_quad(P.A + r * P.lda + kq, r < P.m, P.k - kq, &ra[h * 4]);
+      } else {                                        // (k row, row quad): A stored k x m
+        const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
+        const int64_t kk = k0 + ak, rq = row0 + ar;
+        load_quad(P.A + kk * P.lda + rq, kk < P.k, P.m - rq, &ra[h * 4]);
+      }
     }
 #pragma unroll
     for (int h = 0; h < BQ; h++) {
@@ -168,9 +174,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     for (int h = 0; h < AQ; h++) {
       const int e = tid + h * NTHR;
       if (e >= C::AQN) break;
-      const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
+      if (!P.transa) {
+        const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
 #pragma unroll
-      for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+        for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+      } else {
+        const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; q++) S.a[buf][ak][ar + q] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+      }
     }
 #pragma unroll
     for (int h = 0; h < BQ; h++) {
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           const int64_t r = row0 + ty * TM + i, cc = col0 + tx * TN + j;
           if (r < P.m && cc < P.n) {
             const uint4 o = slow_slab(acc[i][j].M, acc[i][j].E, acc[i][j].sg, P.A, P.lda, P.B, P.ldb, P.neg, r, cc,
-                                      k0, kmax, TRANS_B ? 1 : 0);
+                                      k0, kmax, TRANS_B ? 1 : 0, P.transa);
             acc[i][j].M = o.x; acc[i][j].E = (int32_t)o.y; acc[i][j].sg = (int32_t)o.z; bad = bad | (o.w != 0u);
           }
         }
@@ -263,7 +275,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     // recompute this thread's outputs from scratch with the generic path
     for (int e = 0; e < TM * TN; e++) {
       const int64_t r = row0 + ty * TM + e / TN, cc = col0 + tx * TN + e % TN;
-      if (r < P.m && cc < P.n && (!SYRK || cc <= r)) P.C[r * P.ldc + cc] = slow_chain(P.A, P.lda, P.B, P.ldb, P.C, P.ldc, P.beta, P.neg, P.k, r, cc, TRANS_B ? 1 : 0);
+      if (r < P.m && cc < P.n && (!SYRK || cc <= r)) P.C[r * P.ldc + cc] = slow_chain(P.A, P.lda, P.B, P.ldb, P.C, P.ldc, P.beta, P.neg, P.k, r, cc, TRANS_B ? 1 : 0,
+                                            P.transa);
     }
     return;
   }
@@ -285,7 +298,7 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
   if (P.stop != nullptr && *P.stop != 0) return;
   uint32_t c = P.beta ? P.C[r * P.ldc + cc] : 0u;
   for (int64_t l = 0; l < P.k; l++) {
-    const uint32_t a = P.A[r * P.lda + l];
+    const uint32_t a = P.transa ? P.A[l * P.lda + r] : P.A[r * P.lda + l];
     const uint32_t b = transb ? P.B[cc * P.ldb + l] : P.B[l * P.ldb + cc];
     c = mac_generic(c, a, b, P.neg);
   }

@@ -51,6 +51,7 @@ struct Params {
   int beta;       // 0 or 1
   const int32_t* stop;   // optional device flag: nonzero -> the kernel is a no-op (potrf after a failure)
   int one = 1;           // the constant 1, passed at run time (keeps IMADs on the FMA pipe)
+  int transa = 0;        // op(A) = A^T: A is stored k x m (the four transpose variants)
 };
 
 // ---- staging decode --------------------------------------------------------

@@ -18,11 +18,11 @@ def _pats(x):
     return O.from_f64_array(x)
 
 
-def _gpu_gemm(A, B, C, transb="N", alpha=MONE, beta=ONE, naive=False):
+def _gpu_gemm(A, B, C, transb="N", alpha=MONE, beta=ONE, naive=False, transa="N"):
     import paper_2401_14117_b200 as PB
     dA, dB, dC = to_dev(A), to_dev(B), to_dev(C)
     f = PB.posit_gemm_naive if naive else PB.posit_gemm
-    f(dA, dB, dC, transb=transb, alpha=alpha, beta=beta)
+    f(dA, dB, dC, transb=transb, alpha=alpha, beta=beta, transa=transa)
     return to_host(dC)
 
 
@@ -39,6 +39,22 @@ def test_gemm_matches_oracle(cuda_ok, m, n, k, transb):
     ref = O.gemm(A, B, C, transb=transb)
     assert mismatch(_gpu_gemm(A, B, C, transb), ref) == 0
     assert mismatch(_gpu_gemm(A, B, C, transb, naive=True), ref) == 0
+
+
+@pytest.mark.parametrize("m,n,k", [(3, 5, 7), (67, 131, 45), (200, 129, 300)])
+@pytest.mark.parametrize("transa", ["N", "T"])
+@pytest.mark.parametrize("transb", ["N", "T"])
+def test_gemm_four_transpose_variants(cuda_ok, m, n, k, transa, transb):
+    # Eq.2 with op(X) in {X, X^T}: A stored m x k or k x m, B k x n or n x k
+    A, B, C = SI.config2(n=n, m=m, k=k)
+    if transa == "T":
+        A = A.T.copy()
+    if transb == "T":
+        B = B.T.copy()
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    ref = O.gemm(A, B, C, transa=transa, transb=transb)
+    assert mismatch(_gpu_gemm(A, B, C, transb, transa=transa), ref) == 0
+    assert mismatch(_gpu_gemm(A, B, C, transb, transa=transa, naive=True), ref) == 0
 
 
 @pytest.mark.parametrize("alpha,beta", [(ONE, ONE), (ONE, 0), (MONE, 0)])
