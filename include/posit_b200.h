@@ -84,6 +84,21 @@ int posit_gemm(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32
                const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
                uint32_t* C, int64_t ldc, void* stream);
 
+/*
+ * posit_gemm_eq2 -- Eq.2 for ANY alpha, beta in the order SPEC S:200 states:
+ *   t = sum_l op(A)_il (x) op(B)_lj   accumulated from 0 in ascending l,
+ *   C_ij <- (alpha (x) t) (+) (beta (x) C_ij)   (mul, mul, add),
+ * every operation one correctly rounded Posit(32,2) op.  (posit_gemm keeps the
+ * path's order, reading Q6: c <- c (-) a (x) b from C_ij; for alpha = -1,
+ * beta = 1 the two orders round differently.)  work: DEVICE buffer of
+ * posit_gemm_eq2_work_bytes(m, n) bytes for t (else -15).  Arguments and
+ * layouts as posit_gemm.
+ */
+size_t posit_gemm_eq2_work_bytes(int64_t m, int64_t n);
+int posit_gemm_eq2(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+                   const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
+                   uint32_t* C, int64_t ldc, void* work, size_t work_bytes, void* stream);
+
 /* Same contract and result as posit_gemm, computed by a one-thread-per-output
  * kernel with the generic per-operation path (a parity cross-check; slow). */
 int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,

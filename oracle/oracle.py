@@ -66,6 +66,8 @@ def lib() -> ctypes.CDLL:
             L.or_roundtrip_all32.restype = ctypes.c_int64
             L.or_gemm.argtypes = [ctypes.c_char, ctypes.c_char, i64, i64, i64, u32, vp, i64, vp, i64, u32, vp, i64]
             L.or_gemm.restype = i32
+            L.or_gemm_eq2.argtypes = [ctypes.c_char, ctypes.c_char, i64, i64, i64, u32, vp, i64, vp, i64, u32, vp, i64]
+            L.or_gemm_eq2.restype = i32
             L.or_syrk_lower.argtypes = [i64, i64, u32, vp, i64, u32, vp, i64]
             L.or_syrk_lower.restype = i32
             L.or_trsm_llnu.argtypes = [i64, i64, vp, i64, vp, i64]
@@ -149,6 +151,20 @@ def gemm(A, B, C=None, transa="N", transb="N", alpha=P32_MONE, beta=P32_ONE) -> 
                        _ptr(B), B.shape[1], beta, _ptr(C), max(n, 1))
     if rc != 0:
         raise ValueError(f"or_gemm returned {rc}")
+    return C
+
+
+def gemm_eq2(A, B, C, alpha, beta, transa="N", transb="N") -> np.ndarray:
+    """Eq.2 in SPEC S:200's order: t = sum of products from 0, then (alpha t) + (beta C)."""
+    A, B = _u32(A), _u32(B)
+    m = A.shape[0] if transa == "N" else A.shape[1]
+    k = A.shape[1] if transa == "N" else A.shape[0]
+    n = B.shape[1] if transb == "N" else B.shape[0]
+    C = _u32(C).copy()
+    rc = lib().or_gemm_eq2(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), A.shape[1],
+                           _ptr(B), B.shape[1], beta, _ptr(C), max(n, 1))
+    if rc != 0:
+        raise ValueError(f"or_gemm_eq2 returned {rc}")
     return C
 
 

@@ -352,6 +352,33 @@ int or_gemm(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t 
 }
 
 /* C_lower <- beta*C + alpha * A * A^T (trans 'N': A is n x k).  Upper untouched. */
+/* Eq.2 in the order SPEC S:200 states for general alpha, beta:
+ *   t = sum_l op(A)_il (x) op(B)_lj   accumulated from 0 in ascending l,
+ *   C_ij <- (alpha (x) t) (+) (beta (x) C_ij)   (mul, mul, add; the beta term last).
+ * (posit_gemm's path contract, Q6, is the other order: c <- c (-) a (x) b.) */
+int or_gemm_eq2(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+                const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,
+                uint32_t* C, int64_t ldc) {
+    if (transa != 'N' && transa != 'T') return -1;
+    if (transb != 'N' && transb != 'T') return -2;
+    if (m < 0) return -3;
+    if (n < 0) return -4;
+    if (k < 0) return -5;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t i = 0; i < m; i++) {
+        for (int64_t j = 0; j < n; j++) {
+            uint32_t t = 0u;
+            for (int64_t l = 0; l < k; l++) {
+                const uint32_t a = transa == 'N' ? A[i * lda + l] : A[l * lda + i];
+                const uint32_t b = transb == 'N' ? B[l * ldb + j] : B[j * ldb + l];
+                t = padd(t, pmul(a, b));
+            }
+            C[i * ldc + j] = padd(pmul(alpha, t), pmul(beta, C[i * ldc + j]));
+        }
+    }
+    return 0;
+}
+
 int or_syrk_lower(int64_t n, int64_t k, uint32_t alpha, const uint32_t* A, int64_t lda,
                   uint32_t beta, uint32_t* C, int64_t ldc) {
     if (n < 0) return -3;

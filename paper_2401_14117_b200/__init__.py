@@ -17,7 +17,7 @@ import ctypes
 import os
 
 __all__ = [
-    "lib", "PositError", "posit_gemm", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
+    "lib", "PositError", "posit_gemm", "posit_gemm_eq2", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
     "posit_getrf", "posit_getrf_panel", "posit_getrs", "posit_potrs", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
     "posit_vec_op", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
 ]
@@ -48,6 +48,9 @@ def lib() -> ctypes.CDLL:
         L.posit_gemm.argtypes = gemm_args
         L.posit_gemm_naive.argtypes = gemm_args
         L.posit_gemm_host.argtypes = gemm_args[:-1] + [vp, sz, vp]
+        L.posit_gemm_eq2.argtypes = gemm_args[:-1] + [vp, sz, vp]
+        L.posit_gemm_eq2_work_bytes.argtypes = [i64, i64]
+        L.posit_gemm_eq2_work_bytes.restype = sz
         L.posit_gemm_host_work_bytes.argtypes = [i64, i64, i64]
         L.posit_gemm_host_work_bytes.restype = sz
         L.posit_syrk.argtypes = [c_char, c_char, i64, i64, u32, vp, i64, u32, vp, i64, vp]
@@ -110,6 +113,17 @@ def posit_gemm(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = 
     k = A.shape[1] if transa == "N" else A.shape[0]
     _check(lib().posit_gemm(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B), beta,
                             _ptr(C), _ld(C), _stream(stream)), "posit_gemm")
+
+
+def posit_gemm_eq2(A, B, C, alpha: int, beta: int, transb: str = "N", transa: str = "N", stream=None,
+                   work=None) -> None:
+    """Eq.2 for any alpha, beta (posit patterns) in SPEC S:200's order: t = sum of products, then
+    C <- alpha t + beta C (see include/posit_b200.h)."""
+    m, n = C.shape
+    k = A.shape[1] if transa == "N" else A.shape[0]
+    w, wb = _work(int(lib().posit_gemm_eq2_work_bytes(m, n)), C, work)
+    _check(lib().posit_gemm_eq2(transa.encode(), transb.encode(), m, n, k, alpha, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                beta, _ptr(C), _ld(C), _ptr(w), wb, _stream(stream)), "posit_gemm_eq2")
 
 
 def posit_gemm_naive(A, B, C, transb: str = "N", alpha: int = POSIT_MONE, beta: int = POSIT_ONE, stream=None,

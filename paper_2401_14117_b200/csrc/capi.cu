@@ -80,6 +80,39 @@ int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, 
   return gemm_common(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, true);
 }
 
+size_t posit_gemm_eq2_work_bytes(int64_t m, int64_t n) {
+  if (m < 0 || n < 0) return 0;
+  return (size_t)4 * (size_t)(m * n);
+}
+
+int posit_gemm_eq2(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+                   int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc, void* work,
+                   size_t work_bytes, void* stream) {
+  if (transa != 'N' && transa != 'T') return -1;
+  if (transb != 'N' && transb != 'T') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  const int64_t acols = transa == 'N' ? k : m;
+  if (lda < (acols > 1 ? acols : 1)) return -8;
+  if (ldb < ((transb == 'N' ? n : k) > 1 ? (transb == 'N' ? n : k) : 1)) return -10;
+  if (ldc < (n > 1 ? n : 1)) return -13;
+  if (m == 0 || n == 0) return 0;
+  if (work == nullptr || work_bytes < posit_gemm_eq2_work_bytes(m, n)) return -15;
+  if ((k > 0 && (A == nullptr || B == nullptr)) || C == nullptr) return -7;
+  uint32_t* T = static_cast<uint32_t*>(work);
+  // t = sum of products from 0 (the fast kernel with alpha = +1, beta = 0), then the epilogue
+  int rc;
+  if (k > 0) {
+    pg::Params P{m, n, k, A, lda, B, ldb, T, n, 0, 0, nullptr};
+    P.transa = transa == 'T' ? 1 : 0;
+    if ((rc = pb_launch_gemm(P, transb == 'T', false, S(stream)))) return launch_check(rc);
+  } else if ((rc = cuda_check(cudaMemsetAsync(T, 0, posit_gemm_eq2_work_bytes(m, n), S(stream))))) {
+    return rc;
+  }
+  return launch_check(pb_axpby(alpha, T, n, beta, C, ldc, m, n, S(stream)));
+}
+
 size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k) {
   if (m < 0 || n < 0 || k < 0) return 0;
   return (size_t)4 * (size_t)(m * k + k * n + m * n) + 256;

@@ -738,6 +738,15 @@ __global__ void k_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t*
   }
 }
 
+// C <- (alpha (x) T) (+) (beta (x) C), elementwise (the Eq.2 epilogue, SPEC S:200 order)
+__global__ void k_axpby(uint32_t alpha, const uint32_t* T, int64_t ldt, uint32_t beta, uint32_t* C, int64_t ldc,
+                        int64_t m, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    C[i * ldc + j] = add(mul(alpha, T[i * ldt + j]), mul(beta, C[i * ldc + j]));
+  }
+}
+
 __global__ void k_from_f64(const double* x, uint32_t* out, int64_t count) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = p32::from_f64(x[i]);
@@ -963,6 +972,14 @@ int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64
   if (count <= 0) return 0;
   pb_count_launch();
   k_vec_op<<<grid_for(count, 256), 256, 0, st>>>(op, a, b, out, count);
+  return last_launch();
+}
+
+int pb_axpby(uint32_t alpha, const uint32_t* T, int64_t ldt, uint32_t beta, uint32_t* C, int64_t ldc, int64_t m,
+             int64_t n, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  pb_count_launch();
+  k_axpby<<<grid_for(m * n, 256), 256, 0, st>>>(alpha, T, ldt, beta, C, ldc, m, n);
   return last_launch();
 }
 

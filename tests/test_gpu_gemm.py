@@ -146,3 +146,19 @@ def test_gemm_fast_path_range_boundaries(cuda_ok, ea, ec):
     C = np.ldexp(rng.standard_normal((m, n)), ec + rng.integers(-3, 4, (m, n)))
     A, B, C = _pats(A), _pats(B), _pats(C)
     assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
+
+
+@pytest.mark.parametrize("transa,transb", [("N", "N"), ("T", "N"), ("N", "T")])
+@pytest.mark.parametrize("alpha,beta", [(2.5, 0.75), (-3.0, 1.0), (1.0, 0.0), (0.1, -2.0), (-1.0, 1.0)])
+def test_gemm_eq2_general_alpha_beta(cuda_ok, transa, transb, alpha, beta):
+    import paper_2401_14117_b200 as PB
+    A, B, C = SI.config2(n=130, m=70, k=45)
+    if transa == "T":
+        A = A.T.copy()
+    if transb == "T":
+        B = B.T.copy()
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    a, b = O.from_f64(alpha), O.from_f64(beta)
+    dC = to_dev(C)
+    PB.posit_gemm_eq2(to_dev(A), to_dev(B), dC, a, b, transb=transb, transa=transa)
+    assert mismatch(to_host(dC), O.gemm_eq2(A, B, C, a, b, transa=transa, transb=transb)) == 0

@@ -329,3 +329,24 @@ def test_getrs_potrs_match_checker_brute_force():
     Lc, _ = O.potrf_lower(S)
     y = _checker_fwd(Lc, b, unit=False)
     assert list(O.potrs_lower(Lc, b)) == _checker_back_desc(Lc.T.copy(), y)
+
+
+def test_gemm_eq2_general_alpha_beta_vs_checker():
+    # Eq.2 in SPEC S:200's order, brute force with exact-rational ops
+    rng = np.random.default_rng(77)
+    m, n, k = 3, 4, 5
+    A = P(rng.standard_normal((m, k)))
+    B = P(rng.standard_normal((k, n)))
+    C = P(rng.standard_normal((m, n)))
+    for alpha, beta in [(2.5, 0.75), (-3.0, 1.0), (1.0, 0.0), (0.1, -2.0)]:
+        a, b = O.from_f64(alpha), O.from_f64(beta)
+        got = O.gemm_eq2(A, B, C, a, b)
+        for i in range(m):
+            for j in range(n):
+                t = 0
+                for l in range(k):
+                    t = X.add(t, X.mul(int(A[i, l]), int(B[l, j])))
+                assert int(got[i, j]) == X.add(X.mul(a, t), X.mul(b, int(C[i, j])))
+    # alpha = 1, beta = 0 -> the plain product
+    got = O.gemm_eq2(P([[1.0, 2.0], [3.0, 4.0]]), P([[5.0, 6.0], [7.0, 8.0]]), np.zeros((2, 2), np.uint32), ONE, 0)
+    assert np.array_equal(F(got), [[19.0, 22.0], [43.0, 50.0]])
