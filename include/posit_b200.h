@@ -202,6 +202,18 @@ int posit_getrs(char trans, int64_t n, const uint32_t* LU, int64_t lda, const in
                 void* stream);
 int posit_potrs(char uplo, int64_t n, const uint32_t* L, int64_t lda, uint32_t* b, void* stream);
 
+/*
+ * posit_iamax_key -- pivot search over m entries col[i * stride] whose rows
+ * have global indices global_row[i] (DEVICE int32; the rows a rank owns in a
+ * 2D block-cyclic layout): *key (DEVICE int64) <- max over i with
+ * global_row[i] >= row_min of ((abs(col_i) + 2^31) << 31) | (2^31 - 1 -
+ * global_row[i]), abs by two's complement compared as a signed int (reading
+ * Q10: larger abs first, ties -> smaller row; NaR the minimum), 0 if none.
+ * Non-negative, so a MAX all-reduce over ranks yields the global pivot.
+ */
+int posit_iamax_key(int64_t m, const uint32_t* col, int64_t stride, const int32_t* global_row, int64_t row_min,
+                    int64_t* key, void* stream);
+
 /* Conversions: binary64 -> posit rounds once (RNE), NaN/Inf -> NaR,
  * -0 -> 0, subnormals -> +-minpos; posit -> binary64 is exact (NaR -> NaN). */
 int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream);

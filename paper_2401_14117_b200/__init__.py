@@ -19,7 +19,7 @@ import os
 __all__ = [
     "lib", "PositError", "posit_gemm", "posit_gemm_eq2", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
     "posit_getrf", "posit_getrf_panel", "posit_getrs", "posit_potrs", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
-    "posit_vec_op", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
+    "posit_vec_op", "posit_iamax_key", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
 ]
 
 POSIT_ONE = 0x40000000
@@ -65,6 +65,7 @@ def lib() -> ctypes.CDLL:
         L.posit_potrf_work_bytes.restype = sz
         L.posit_getrs.argtypes = [c_char, i64, vp, i64, vp, vp, vp]
         L.posit_potrs.argtypes = [c_char, i64, vp, i64, vp, vp]
+        L.posit_iamax_key.argtypes = [i64, vp, i64, vp, i64, vp, vp]
         L.posit_from_f64.argtypes = [vp, vp, i64, vp]
         L.posit_to_f64.argtypes = [vp, vp, i64, vp]
         L.posit_vec_op.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp]
@@ -207,6 +208,15 @@ def posit_potrs(L, b, stream=None) -> None:
     """b <- A^{-1} b in place with the posit_potrf lower factor (one RHS, device tensors)."""
     n = L.shape[0]
     _check(lib().posit_potrs(b"L", n, _ptr(L), _ld(L), _ptr(b), _stream(stream)), "posit_potrs")
+
+
+def posit_iamax_key(col, global_row, row_min: int, key, stream=None) -> None:
+    """key (int64 device tensor, 1) <- pivot key of the strided column view col (m x 1 or m) over rows
+    whose global index (int32 device tensor, m) is >= row_min (see include/posit_b200.h)."""
+    m = col.shape[0]
+    stride = col.stride(0)
+    _check(lib().posit_iamax_key(m, _ptr(col), stride, _ptr(global_row), row_min, _ptr(key), _stream(stream)),
+           "posit_iamax_key")
 
 
 def posit_from_f64(x, out=None, stream=None):

@@ -396,6 +396,15 @@ int posit_potrs(char uplo, int64_t n, const uint32_t* L, int64_t lda, uint32_t* 
   return launch_check(pb_solve(true, n, L, lda, nullptr, b, S(stream)));
 }
 
+int posit_iamax_key(int64_t m, const uint32_t* col, int64_t stride, const int32_t* global_row, int64_t row_min,
+                    int64_t* key, void* stream) {
+  if (m < 0) return -1;
+  if (stride < 1) return -3;
+  if (key == nullptr) return -7;
+  if (m > 0 && (col == nullptr || global_row == nullptr)) return -2;
+  return launch_check(pb_iamax_key(m, col, stride, global_row, row_min, reinterpret_cast<long long*>(key), S(stream)));
+}
+
 int posit_from_f64(const double* x, uint32_t* out, int64_t count, void* stream) {
   if (count < 0) return -3;
   return launch_check(pb_from_f64(x, out, count, S(stream)));

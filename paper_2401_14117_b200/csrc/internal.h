@@ -24,6 +24,8 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
 int pb_solve(bool chol, int64_t n, const uint32_t* A, int64_t lda, const int32_t* ipiv, uint32_t* b, cudaStream_t st);
 int pb_axpby(uint32_t alpha, const uint32_t* T, int64_t ldt, uint32_t beta, uint32_t* C, int64_t ldc, int64_t m,
              int64_t n, cudaStream_t st);
+int pb_iamax_key(int64_t m, const uint32_t* col, int64_t stride, const int32_t* grow, int64_t row_min, long long* out,
+                 cudaStream_t st);
 int pb_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, cudaStream_t st);
 int pb_from_f64(const double* x, uint32_t* out, int64_t count, cudaStream_t st);
 int pb_to_f64(const uint32_t* p, double* out, int64_t count, cudaStream_t st);

@@ -220,6 +220,26 @@ __global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, in
   for (int e = tid; e < nr * W; e += NT) A[(rb + e / W) * lda + e % W] = tile[e];
 }
 
+// Pivot key over a strided column whose rows carry global indices (the 2D
+// block-cyclic panel, where a rank's rows are not contiguous): max over rows
+// with grow[i] >= row_min of  ((abs(a) + 2^31) << 31) | (2^31 - 1 - grow[i]),
+// i.e. larger abs first, then the smaller global row (reading Q10), as a
+// non-negative int64 suitable for a MAX all-reduce.  0 if no row qualifies.
+__global__ void __launch_bounds__(1024) k_iamax_key(int64_t m, const uint32_t* col, int64_t stride,
+                                                    const int32_t* grow, int64_t row_min, long long* out) {
+  __shared__ unsigned long long red[32];
+  unsigned long long best = 0ull;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t g = grow[i];
+    if (g < row_min) continue;
+    const uint64_t a = (uint64_t)((int64_t)abs_key(col[i * stride]) + 2147483648ll);
+    const unsigned long long k = (a << 31) | (uint64_t)(2147483647ll - g);
+    best = k > best ? k : best;
+  }
+  best = block_max(best, red);
+  if (threadIdx.x == 0) *out = (long long)best;
+}
+
 // laswp: rows k1..k2-1 swapped with ipiv[k]-1-base, in order, on columns
 // [0, ncols).  One CTA per 32 columns.  Instead of walking the swaps through
 // global memory (a dependent load/store chain per swap), the CTA gathers every
@@ -965,6 +985,13 @@ int pb_solve(bool chol, int64_t n, const uint32_t* A, int64_t lda, const int32_t
   pb_count_launch();
   if (chol) k_potrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, b);
   else k_getrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, ipiv, b);
+  return last_launch();
+}
+
+int pb_iamax_key(int64_t m, const uint32_t* col, int64_t stride, const int32_t* grow, int64_t row_min, long long* out,
+                 cudaStream_t st) {
+  pb_count_launch();
+  k_iamax_key<<<1, 1024, 0, st>>>(m, col, stride, grow, row_min, out);
   return last_launch();
 }
 

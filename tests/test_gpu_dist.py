@@ -91,3 +91,48 @@ def test_potrf_dist_emulated_ranks_cuda(cuda_ok, P):
     ref, rinfo = O.potrf_lower(A)
     il = np.tril_indices(n)
     assert mismatch(got[il], ref[il]) == 0 and all(int(i.cpu()[0]) == rinfo for i in infos)
+
+
+def test_iamax_key_cuda(cuda_ok):
+    import paper_2401_14117_b200 as PB
+    rng = np.random.default_rng(9)
+    pats = O.from_f64_array(SI.normal_matrix((300, 5), 1.0, 9))
+    pats[17, 2] = O.P32_NAR
+    pats[40, 2] = pats[41, 2]                     # a tie in |a|
+    col = to_dev(pats)[:, 2]
+    grow = torch.from_numpy(rng.permutation(1000)[:300].astype(np.int32)).cuda()
+    key = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for row_min in (0, 400, 900, 2000):
+        PB.posit_iamax_key(col, grow, row_min, key)
+        x = pats[:, 2].astype(np.int64)
+        s = np.where(x >= 2 ** 31, x - 2 ** 32, x)
+        a = np.where(s < 0, -s, s)
+        a = np.where(s == -(2 ** 31), -(2 ** 31), a)
+        g = grow.cpu().numpy().astype(np.int64)
+        ok = g >= row_min
+        ref = int((((a[ok] + 2 ** 31) << 31) | ((2 ** 31 - 1) - g[ok])).max()) if ok.any() else 0
+        assert int(key.item()) == ref
+
+
+def test_getrf_dist2d_1x1_cuda(cuda_ok):
+    import socket
+    import torch.distributed as dist
+    from paper_2401_14117_b200.dist2d import BlockCyclic2D, Groups, getrf_dist2d
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        n, nb = 150, 16
+        A = O.from_f64_array(SI.config4(n))
+        desc = BlockCyclic2D(n, nb, 1, 1, 0, 0)
+        loc = desc.scatter(to_dev(A))
+        ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+        getrf_dist2d(loc, desc, ipiv, info, Groups(1, 1))
+        ref, rpiv, rinfo = O.getrf(A)
+        assert mismatch(to_host(loc), ref) == 0
+        assert np.array_equal(ipiv.cpu().numpy(), rpiv) and int(info.cpu()[0]) == rinfo
+    finally:
+        dist.destroy_process_group()
