@@ -13,6 +13,9 @@
 namespace pg {
 
 constexpr int KK_UNROLL = PG_KK_UNROLL;   // k-steps of the fast loop unrolled (each TM x TN MACs)
+#ifndef PG_CPASYNC
+#define PG_CPASYNC 0
+#endif
 #ifndef PG_GROUP_M
 #define PG_GROUP_M 32
 #endif
@@ -32,6 +35,10 @@ struct Cfg {
   struct Smem {
     uint4 a[2][BK][BM];
     uint4 b[2][BK][BN];
+#if PG_CPASYNC
+    uint32_t ra[BM * BK];                 // raw patterns of the next slab (cp.async target, by quad)
+    uint32_t rb[BK * BN];
+#endif
     uint4 tp[TSIZE];
     uint4 tx[TSIZE];
   };
@@ -88,6 +95,20 @@ __device__ __forceinline__ void load_quad(const uint32_t* p, bool row_ok, int64_
   } else {
 #pragma unroll
     for (int q = 0; q < 4; q++) out[q] = (row_ok && q < avail) ? __ldg(p + q) : p32::ONE;
+  }
+}
+
+// cp.async of one quad into shared memory (16 B when complete and aligned,
+// else word by word; slots past the matrix are left untouched and replaced by
+// 1.0 at decode time)
+__device__ __forceinline__ void cp_quad(uint32_t* dst, const uint32_t* p, bool row_ok, int64_t avail) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  if (row_ok && avail >= 4 && (((uintptr_t)p) & 15u) == 0u) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(p));
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (row_ok && q < avail) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4u * q), "l"(p + q));
   }
 }
 
@@ -201,16 +222,108 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
     return sp;
   };
 
+
+#if PG_CPASYNC
+  // cp.async staging: each thread copies its own quads of the next slab into
+  // the raw buffers and later decodes exactly those quads (no cross-thread
+  // dependency on the raw data, so only its own wait_group is needed)
+  auto issue_tile = [&](int64_t k0) {
+#pragma unroll
+    for (int h = 0; h < AQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::AQN) break;
+      if (!P.transa) {
+        const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
+        const int64_t r = row0 + ar, kq = k0 + ak;
+        cp_quad(&S.ra[e * 4], P.A + r * P.lda + kq, r < P.m, P.k - kq);
+      } else {
+        const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
+        const int64_t kk = k0 + ak, rq = row0 + ar;
+        cp_quad(&S.ra[e * 4], P.A + kk * P.lda + rq, kk < P.k, P.m - rq);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < BQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::BQN) break;
+      if (!TRANS_B) {
+        const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
+        const int64_t kk = k0 + bk, cq = col0 + bc;
+        cp_quad(&S.rb[e * 4], P.B + kk * P.ldb + cq, kk < P.k, P.n - cq);
+      } else {
+        const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
+        const int64_t kq = k0 + bk, cc = col0 + bc;
+        cp_quad(&S.rb[e * 4], P.B + cc * P.ldb + kq, cc < P.n, P.k - kq);
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  auto decode_tile = [&](int buf, int64_t k0) -> uint32_t {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    uint32_t sp = 0u;
+#pragma unroll
+    for (int h = 0; h < AQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::AQN) break;
+      if (!P.transa) {
+        const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
+        const bool rok = row0 + ar < P.m;
+        const int64_t av = P.k - (k0 + ak);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          S.a[buf][ak + q][ar] = stage_decode<31>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+      } else {
+        const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
+        const bool rok = k0 + ak < P.k;
+        const int64_t av = P.m - (row0 + ar);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          S.a[buf][ak][ar + q] = stage_decode<31>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < BQ; h++) {
+      const int e = tid + h * NTHR;
+      if (e >= C::BQN) break;
+      if (!TRANS_B) {
+        const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
+        const bool rok = k0 + bk < P.k;
+        const int64_t av = P.n - (col0 + bc);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          S.b[buf][bk][bc + q] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp);
+      } else {
+        const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
+        const bool rok = col0 + bc < P.n;
+        const int64_t av = P.k - (k0 + bk);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          S.b[buf][bk + q][bc] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp);
+      }
+    }
+    return sp;
+  };
+#endif
+
   const int64_t ntiles = (P.k + BK - 1) / BK;
+#if PG_CPASYNC
+  if (ntiles > 0) issue_tile(0);
+  int special = ntiles > 0 ? __syncthreads_or((int)decode_tile(0, 0)) : 0;
+#else
   if (ntiles > 0) {
     load_tile(0);
   }
   int special = ntiles > 0 ? __syncthreads_or((int)store_tile(0)) : 0;
+#endif
 
   for (int64_t t = 0; t < ntiles; t++) {
     const int cur = (int)(t & 1);
     const int64_t k0 = t * BK;
+#if PG_CPASYNC
+    if (t + 1 < ntiles) issue_tile(k0 + BK);
+#else
     if (t + 1 < ntiles) load_tile(k0 + BK);
+#endif
     const int kmax = (int)min((int64_t)BK, P.k - k0);
     if (!special) {
       // the accumulators must start the slab within the range that keeps every
@@ -267,7 +380,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         }
       }
     }
+#if PG_CPASYNC
+    if (t + 1 < ntiles) special = __syncthreads_or((int)decode_tile(cur ^ 1, k0 + BK));
+#else
     if (t + 1 < ntiles) special = __syncthreads_or((int)store_tile(cur ^ 1));
+#endif
   }
 
   // ---- epilogue ------------------------------------------------------------
