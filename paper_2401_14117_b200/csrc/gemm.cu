@@ -7,14 +7,14 @@
 #include "internal.h"
 
 #ifndef PG_KK_UNROLL
-#define PG_KK_UNROLL 1
+#define PG_KK_UNROLL 2
 #endif
 
 namespace pg {
 
 constexpr int KK_UNROLL = PG_KK_UNROLL;   // k-steps of the fast loop unrolled (each TM x TN MACs)
 #ifndef PG_CPASYNC
-#define PG_CPASYNC 0
+#define PG_CPASYNC 1
 #endif
 #ifndef PG_GROUP_M
 #define PG_GROUP_M 32
