@@ -105,6 +105,17 @@ def _load_json(path):
 
 
 # ---------------------------------------------------------------- reference arm
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_oracle_sample(workload: str, target_s: float = 12.0):
     """Time the oracle (as it stands) on a bounded sample of the workload."""
     from oracle import oracle as O
@@ -125,7 +136,7 @@ def cpu_oracle_sample(workload: str, target_s: float = 12.0):
         flops = 2.0 * rows * 4096 * 4096
         return {"value": flops / dt / 1e9, "unit": "Gflop/s", "cores": cores, "kind": "oracle",
                 "sample": f"{rows} of 4096 output rows of configs[1] GEMM (full k=4096 chains), {dt:.1f} s",
-                "seconds": dt}
+                "seconds": dt, "cpu_model": _cpu_model()}
     # LU / Cholesky: the oracle's textbook loop on a leading n_s x n_s sample of the same recipe
     n_s = 256
     while True:
@@ -145,7 +156,8 @@ def cpu_oracle_sample(workload: str, target_s: float = 12.0):
             break
         n_s = int(n_s * 1.26 ** 3)   # ~2x work steps
     return {"value": flops / dt / 1e9, "unit": "Gflop/s", "cores": cores, "kind": "oracle",
-            "sample": f"{workload} of the same recipe at n={n_s} (oracle textbook loop), {dt:.1f} s", "seconds": dt}
+            "sample": f"{workload} of the same recipe at n={n_s} (oracle textbook loop), {dt:.1f} s", "seconds": dt,
+            "cpu_model": _cpu_model()}
 
 
 def run_reference(args):

@@ -18,5 +18,8 @@ $BCMD > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $BCMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 python tools/prof_gemm.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 1 -c 1 -o gpurun_out/prof_gemm_$TAG python tools/prof_gemm.py > gpurun_out/ncu_full_$TAG.log 2>&1
+# the first C4 trailing update (16128^2 x 256), SURVEY 8(d)
+PROF_SHAPE=16128,16128,256 python tools/prof_gemm.py > gpurun_out/prof_plain_c4_$TAG.log 2>&1 && \
+PROF_SHAPE=16128,16128,256 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 1 -c 1 -o gpurun_out/prof_gemm_c4_$TAG python tools/prof_gemm.py > gpurun_out/ncu_full_c4_$TAG.log 2>&1
 fi
 echo done
