@@ -407,6 +407,151 @@ __global__ void __launch_bounds__(1024) k_trsm_llnu_blk(const uint32_t* L, int64
   if (wid < ib && c0 + lane < n) B[(i0 + wid) * ldb + c0 + lane] = sb[wid][lane];
 }
 
+// The same in-block solve with one thread per column of B (default).  Columns
+// are independent, so a thread runs its column's substitution alone: rows in
+// groups of LC_G, each group first taking the updates from every earlier
+// (final) row of the block in ascending k -- LC_G independent MAC chains -- and
+// then the in-group triangle, still ascending k per element (Q6).  No shuffles
+// and no idle lanes.  The MACs run branch-free in k-slabs of <= 16 (the
+// GEMM's exactness argument, csrc/gemm.cuh: operands |E| <= 37, accumulators
+// |E| <= 75 at the slab start); a slab whose operands or accumulators fall
+// outside runs the generic pattern path instead.  L's 32 x 32 block is staged
+// decoded (read as a broadcast); a column's final rows stay in the thread's
+// own shared slots.
+constexpr int LC_T = 32, LC_SLAB = 16;
+
+__device__ __forceinline__ void lc_renorm(LaneVal& v) {
+  if (v.dec && !(v.a.E <= 75 && v.a.E >= -75) && v.a.E > pg::E_ZERO_LIMIT) {
+    v.pat = pg::acc_encode(v.a);
+    v.dec = false;
+  }
+}
+
+template <int LC_G>
+__global__ void __launch_bounds__(LC_T) k_trsm_llnu_col(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t i0, int64_t ib, int64_t n, int one) {
+  __shared__ uint4 sl[TB][TB];          // L[i0 + r][i0 + c] decoded A-format {M, E, sigma, pattern}
+  __shared__ uint4 sb[TB][LC_T];        // final rows of each thread's column: B-format {M, E, sg, pattern}
+  __shared__ uint32_t ps[LC_G][LC_T];   // generic path: the group's values as patterns
+  __shared__ uint32_t lmask[TB];        // bit c of row r: L[r][c] is a fast operand (rows >= ib: all ones)
+  __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];
+  const int lane = threadIdx.x;
+  const int64_t col = (int64_t)blockIdx.x * LC_T + lane;
+  const bool live = col < n;
+  pg::fill_tables(tp, tx, lane, LC_T);
+  // stage L's block (row r: lane = column, coalesced) and the column's ib
+  // values of B: all loads first (in flight together), then decode L in place
+  // with the fast masks by ballot (a compact loop: this code runs once)
+#pragma unroll
+  for (int r = 0; r < TB; r++) {
+    sl[r][lane].w = r >= ib ? 0x40000000u : (lane < r ? L[(i0 + r) * ldl + i0 + lane] : 0u);   // rows >= ib: dummy 1.0
+    sb[r][lane].w = (live && r < ib) ? B[(i0 + r) * ldb + col] : 0u;     // the input, until row r is final
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int r = 0; r < TB; r++) {
+    const uint32_t x = sl[r][lane].w;
+    uint4 d;
+    const bool f = fast_a(x, d);
+    sl[r][lane] = make_uint4(d.x, d.y, d.z, x);
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+    if (lane == 0) lmask[r] = r >= ib ? 0xFFFFFFFFu : (bal & ((1u << r) - 1u));
+  }
+  pg::MacConst K;
+  K.one = (uint32_t)one;
+  K.sixteen = 16u * K.one;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(tx + pg::TBIAS) - 30u * 16u;
+  __syncthreads();
+  if (!live) return;
+  uint32_t bmask = 0u;                    // bit k: final row k is a fast B operand
+  for (int g0 = 0; g0 < ib; g0 += LC_G) {
+    LaneVal v[LC_G];
+    uint32_t lg = 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < LC_G; u++) {
+      lv_load(v[u], sb[g0 + u][lane].w);
+      lg &= lmask[g0 + u];
+    }
+    // the updates from the final rows k < g0, ascending k, in slabs
+    for (int k0 = 0; k0 < g0; k0 += LC_SLAB) {
+      const int kn = (g0 - k0) < LC_SLAB ? (g0 - k0) : LC_SLAB;
+      const uint32_t sm = ((1u << kn) - 1u) << k0;
+      bool ok = (bmask & sm) == sm && (lg & sm) == sm;
+#pragma unroll
+      for (int u = 0; u < LC_G; u++) ok = ok && v[u].dec;
+      if (ok) {
+        for (int k = k0; k < k0 + kn; k++) {
+          const uint4 bk = sb[k][lane];
+          uint32_t bad = 0u;
+#pragma unroll
+          for (int u = 0; u < LC_G; u++) {
+            const uint4 ad = sl[g0 + u][k];
+            pg::mac<pg::MacConst, false>(v[u].a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bk.x, (int32_t)bk.y,
+                                         -(int32_t)bk.z, K, bad);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) lc_renorm(v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) ps[u][lane] = lv_pattern(v[u]);
+#pragma unroll 1
+        for (int k = k0; k < k0 + kn; k++) {
+          const uint32_t bp = sb[k][lane].w;
+#pragma unroll 1
+          for (int u = 0; u < LC_G; u++) ps[u][lane] = sub(ps[u][lane], mul(sl[g0 + u][k].w, bp));
+        }
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) lv_load(v[u], ps[u][lane]);
+      }
+    }
+    // the in-group triangle: row g0 + u is final once its predecessors are
+    int ugen = LC_G;
+#pragma unroll
+    for (int u = 0; u < LC_G; u++) {
+      if (ugen == LC_G) {
+        const bool opf = lv_operand(v[u]);
+        bool ok = opf;
+#pragma unroll
+        for (int w = u + 1; w < LC_G; w++) ok = ok && v[w].dec && ((lmask[g0 + w] >> (g0 + u)) & 1u);
+        if (!ok) {
+          ugen = u;
+        } else {
+          const uint32_t pat = pg::acc_encode(v[u].a);
+          sb[g0 + u][lane] = make_uint4(v[u].a.M, (uint32_t)v[u].a.E, (uint32_t)v[u].a.sg, pat);
+          bmask |= 1u << (g0 + u);
+          if (g0 + u < ib) B[(i0 + g0 + u) * ldb + col] = pat;
+          uint32_t bad = 0u;
+#pragma unroll
+          for (int w = u + 1; w < LC_G; w++) {
+            const uint4 ad = sl[g0 + w][g0 + u];
+            pg::mac<pg::MacConst, false>(v[w].a, ad.x, (int32_t)ad.y, (int32_t)ad.z, v[u].a.M, v[u].a.E, -v[u].a.sg,
+                                         K, bad);
+          }
+        }
+      }
+    }
+    if (ugen < LC_G) {                    // the rest of the triangle on patterns
+#pragma unroll
+      for (int u = 0; u < LC_G; u++)
+        if (u >= ugen) ps[u][lane] = lv_pattern(v[u]);
+#pragma unroll 1
+      for (int u = ugen; u < LC_G; u++) {
+        const uint32_t pat = ps[u][lane];
+        LaneVal f;
+        lv_load(f, pat);
+        const bool opf = lv_operand(f);
+        sb[g0 + u][lane] = make_uint4(f.a.M, (uint32_t)f.a.E, (uint32_t)f.a.sg, pat);
+        if (opf) bmask |= 1u << (g0 + u);
+        if (g0 + u < ib) B[(i0 + g0 + u) * ldb + col] = pat;
+#pragma unroll 1
+        for (int w = u + 1; w < LC_G; w++) ps[w][lane] = sub(ps[w][lane], mul(sl[g0 + w][g0 + u].w, pat));
+      }
+    }
+  }
+}
+
 // Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 16).
 // Half-warp per row of B (two rows per warp), lane = column (coalesced):
 // step k finalises b_k <- b_k (/) l_kk, broadcasts it within the half-warp,
@@ -900,11 +1045,25 @@ int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, co
 
 int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
+  // thread per column (row groups of 4; -1 = auto) once the columns fill the
+  // SMs: one such launch costs ~46 us whatever its width up to 592 warps,
+  // the warp-per-column kernel ~34 us per wave of 148 CTAs (r02v launch lists)
+  static const int col_env = [] {
+    const char* e = getenv("POSIT_LLNU_COL");
+    const int v = e == nullptr ? -1 : atoi(e);
+    return v == 0 || v == 4 || v == 8 ? v : -1;
+  }();
+  const int use_col = col_env >= 0 ? col_env : (n > 148 * TB ? 4 : 0);
   for (int64_t i0 = 0; i0 < m; i0 += TB) {
     const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
     if (ib > 1) {
       pb_count_launch();
-      k_trsm_llnu_blk<<<(unsigned)((n + TB - 1) / TB), 1024, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+      if (use_col == 8)
+        k_trsm_llnu_col<8><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
+      else if (use_col == 4)
+        k_trsm_llnu_col<4><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
+      else
+        k_trsm_llnu_blk<<<(unsigned)((n + TB - 1) / TB), 1024, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
     }
     if (i0 + ib < m) {
       pg::Params P{m - i0 - ib, n, ib, L + (i0 + ib) * ldl + i0, ldl, B + i0 * ldb, ldb, B + (i0 + ib) * ldb, ldb,

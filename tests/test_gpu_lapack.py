@@ -36,7 +36,7 @@ def _gpu_potrf(A, nb):
 
 def test_trsm_llnu_matches_oracle(cuda_ok):
     import paper_2401_14117_b200 as PB
-    for m, n in [(1, 5), (37, 100), (256, 300)]:
+    for m, n in [(1, 5), (37, 100), (33, 65), (256, 300), (256, 1000)]:
         L = _pats(np.tril(SI.lu_matrix(m, 1), -1) + np.eye(m))
         B = _pats(SI.normal_matrix((m, n), 1.0, 2))
         dB = to_dev(B)
@@ -164,6 +164,7 @@ def test_trsm_extreme_scales_and_zeros(cuda_ok, scale):
     B64 = np.ldexp(SI.normal_matrix((m, n), 1.0, 14), scale)
     B64[:, 7] = 0.0
     B64[10, :] = 0.0
+    B64[12, 40] = np.nan                              # NaR: absorbing down column 40
     L, B = _pats(L64), _pats(B64)
     dB = to_dev(B)
     PB.posit_trsm("L", "L", "N", "U", to_dev(L), dB)
