@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <stdio.h>
+#include <stddef.h>
 #include <cooperative_groups.h>
 #include "gemm.cuh"
 #include "internal.h"
@@ -56,14 +58,84 @@ __device__ __forceinline__ unsigned long long block_max(unsigned long long v, un
   return v;   // valid in thread 0
 }
 
+// ---- decoded lane values for the in-block kernels -----------------------------
+// A value that lives in a register across many posit updates is kept decoded
+// (the GEMM's accumulator format, csrc/gemm.cuh) so that each update
+// c <- c (-) a (x) b runs the decoded-domain MAC (one rounding for the product,
+// one for the difference, as always) instead of decode -> mul -> encode ->
+// decode -> sub -> encode.  Conservative range guards route any update whose
+// operands or result could leave the MAC's exact range (zero / NaR operands,
+// |E| > 37 operands, |E| > 75 values) to the generic pattern path; both are
+// bit-identical by construction.
+struct LaneVal {
+  pg::Acc a;       // decoded (valid when dec)
+  uint32_t pat;    // pattern (valid when !dec)
+  bool dec;
+};
+
+__device__ __forceinline__ void lv_load(LaneVal& v, uint32_t x) {
+  v.pat = x;
+  v.dec = pg::acc_decode(x, v.a) && (x == 0u || (v.a.E <= 75 && v.a.E >= -75));
+}
+
+__device__ __forceinline__ uint32_t lv_pattern(const LaneVal& v) { return v.dec ? pg::acc_encode(v.a) : v.pat; }
+
+// operand view of a lane value: B format (hidden@30), fast iff nonzero and |E| <= 37
+__device__ __forceinline__ bool lv_operand(const LaneVal& v) {
+  return v.dec && v.a.E > -1000 && v.a.E <= 37 && v.a.E >= -37;
+}
+
+// A-format decode of a pattern operand: fast iff nonzero, not NaR, |E| <= 37
+__device__ __forceinline__ bool fast_a(uint32_t x, uint4& d) {
+  uint32_t sp = 0u;
+  d = pg::stage_decode<31>(x, 0u, sp);
+  return sp == 0u && (int32_t)d.y <= 37 && (int32_t)d.y >= -37;
+}
+
+// c <- c (-) a (x) b; a = pattern (with its A-format decode), b = operand lane
+// value broadcast as (M, E, sg) plus its pattern bp.
+__device__ __forceinline__ void lv_fms(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
+                                       int32_t bsg, bool bfast, uint32_t bp) {
+  if (afast && bfast && c.dec) {
+    uint32_t bad = 0u;
+    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, pg::CalcConst(), bad);
+    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
+    if (!c.dec) c.pat = pg::acc_encode(c.a);                 // |E| in (75, 107]: exact, leave the fast range
+  } else {
+    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
+    lv_load(c, r);
+  }
+}
+
+// lv_fms with the GEMM's shared-memory tables (or any table type)
+template <class Tab>
+__device__ __forceinline__ void lv_fms_t(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
+                                         int32_t bsg, bool bfast, uint32_t bp, const Tab& K) {
+  if (afast && bfast && c.dec) {
+    uint32_t bad = 0u;
+    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, K, bad);
+    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
+    if (!c.dec) c.pat = pg::acc_encode(c.a);
+  } else {
+    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
+    lv_load(c, r);
+  }
+}
+
 // ---- LU leaf (column by column, multi-CTA) ----------------------------------
 // Workspace: key[0..w) (uint64, zeroed per leaf) and a CTA counter.
+constexpr int LEAF_MAXCTA = 160;
 struct LeafWs {
   unsigned long long key[64];
   unsigned int done;
   uint32_t rowp[64];       // cooperative leaf: the pivot row and the current row, published
   uint32_t rowj[64];
+  // one-sync cooperative leaf, by column parity: each CTA's best pivot
+  // candidate row for the next column, and the row at the next diagonal position
+  uint32_t cand[2][LEAF_MAXCTA][64];
+  uint32_t jrow[2][64];
 };
+constexpr size_t LEAF_WS_ZERO = offsetof(LeafWs, cand);   // the part zeroed per leaf
 
 // key[0] <- max over rows 0..m-1 of column 0
 __global__ void k_leaf_colmax(const uint32_t* A, int64_t lda, int64_t m, LeafWs* ws) {
@@ -154,9 +226,18 @@ __global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, in
                                                             int64_t row_base, LeafWs* ws) {
   extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
   __shared__ unsigned long long red[32];
+  __shared__ uint4 urow[64];                          // the pivot row as decoded B operands {M, E, sg, fast}
+  __shared__ uint32_t urowp[64];                      // ... and as patterns
+  __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];      // the MAC's constant tables
   const int NT = blockDim.x;
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
+  pg::fill_tables(tp, tx, tid, NT);
+  pg::MacConst K;
+  K.one = 1u;
+  K.sixteen = 16u;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(tx + pg::TBIAS) - 30u * 16u;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t re = (rb + rows_per_cta) < m ? (rb + rows_per_cta) : m;
   const int nr = re > rb ? (int)(re - rb) : 0;
@@ -176,36 +257,66 @@ __global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, in
   const int64_t jmax = m < w ? m : w;
   for (int64_t j = 0; j < jmax; j++) {
     grid.sync();
-    const unsigned long long key = *(volatile unsigned long long*)&ws->key[j];
+    const unsigned long long key = __ldcg(&ws->key[j]);
     const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
     // publish rows p and j
     if (p >= rb && p < re) for (int c = tid; c < W; c += NT) ws->rowp[c] = tile[(p - rb) * W + c];
     if (j >= rb && j < re) for (int c = tid; c < W; c += NT) ws->rowj[c] = tile[(j - rb) * W + c];
     grid.sync();
-    const uint32_t v = ((volatile uint32_t*)ws->rowp)[j];
+    const uint32_t v = __ldcg(ws->rowp + j);
     if (blockIdx.x == 0 && tid == 0) {
       ipiv[j] = (int32_t)(row_base + p + 1);
       if (v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
     }
     if (v != 0u && p != j) {                          // swap rows j and p (whole leaf width)
-      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = ((volatile uint32_t*)ws->rowp)[c];
-      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = ((volatile uint32_t*)ws->rowj)[c];
+      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = __ldcg(ws->rowp + c);
+      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = __ldcg(ws->rowj + c);
     }
     __syncthreads();
-    // divide column j below the diagonal (Q8; skipped for a zero pivot, Q11)
+    // the row now at position j (the pivot row), decoded once as B operands
+    const uint32_t* rowj = (v != 0u && p != j) ? ws->rowp : ws->rowj;
+    for (int c = tid; c < W; c += NT) {
+      LaneVal t;
+      const uint32_t x = __ldcg(rowj + c);                // L2 (written by another CTA before the grid sync)
+      lv_load(t, x);
+      urow[c] = make_uint4(t.a.M, (uint32_t)t.a.E, (uint32_t)t.a.sg, lv_operand(t) ? 1u : 0u);
+      urowp[c] = x;
+    }
+    // divide column j below the diagonal (Q8; skipped for a zero pivot, Q11):
+    // decoded division by the shared divisor, generic outside its range
     const int64_t i0 = (j + 1 > rb ? j + 1 : rb) - rb;
-    if (v != 0u)
-      for (int64_t i = i0 + tid; i < nr; i += NT) tile[i * W + j] = div(tile[i * W + j], v);
+    if (v != 0u) {
+      pg::Acc dv;
+      const bool dok = pg::acc_decode(v, dv) && v != 0x80000000u && dv.E <= 37 && dv.E >= -37;
+      const double rcp = dok ? __drcp_rn((double)dv.M) * 4294967296.0 : 0.0;
+      for (int64_t i = i0 + tid; i < nr; i += NT) {
+        const uint32_t x = tile[i * W + j];
+        LaneVal t;
+        lv_load(t, x);
+        bool done = false;
+        if (dok && t.dec) done = pg::acc_div(t.a, dv.M, dv.E, dv.sg, rcp, K);
+        tile[i * W + j] = done ? pg::acc_encode(t.a) : div(x, v);
+      }
+    }
     __syncthreads();
     // update columns j+1..w-1 of rows j+1..m-1 with row j (= the pivot row), then fold column j+1
     const int wq = W - (int)j - 1;
     unsigned long long best = 0ull;
     if (wq > 0) {
-      const uint32_t* rowj = (v != 0u && p != j) ? ws->rowp : ws->rowj;   // the row now at position j
-      for (int64_t e = tid; e < (nr - i0) * wq; e += NT) {
-        const int64_t i = i0 + e / wq;
-        const int q = (int)j + 1 + (int)(e % wq);
-        const uint32_t nv = sub(tile[i * W + q], mul(tile[i * W + j], ((volatile const uint32_t*)rowj)[q]));
+      const uint32_t cnt = nr > i0 ? (uint32_t)(nr - i0) * (uint32_t)wq : 0u;      // 32-bit index math (rows per CTA are few)
+      for (uint32_t e = tid; e < cnt; e += NT) {
+        const uint32_t ii = e / (uint32_t)wq;
+        const int i = (int)i0 + (int)ii;
+        const int q = (int)j + 1 + (int)(e - ii * (uint32_t)wq);
+        // decoded-domain c (-) l (x) u (generic outside the MAC's exact range)
+        const uint32_t lp = tile[i * W + j];
+        uint4 ad;
+        const bool af = fast_a(lp, ad);
+        const uint4 ub = urow[q];
+        LaneVal c;
+        lv_load(c, tile[i * W + q]);
+        lv_fms_t(c, lp, af, ad, ub.x, (int32_t)ub.y, (int32_t)ub.z, ub.w != 0u, urowp[q], K);
+        const uint32_t nv = lv_pattern(c);
         tile[i * W + q] = nv;
         if (q == j + 1) {
           const unsigned long long k = piv_key(nv, rb + i);
@@ -214,6 +325,139 @@ __global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, in
       }
       best = block_max(best, red);
       if (tid == 0 && best != 0ull) atomicMax(&ws->key[j + 1], best);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * W; e += NT) A[(rb + e / W) * lda + e % W] = tile[e];
+}
+
+// The same leaf with ONE grid sync per column.  Instead of publishing rows j
+// and p after the pivot is known (a second grid sync), every CTA publishes,
+// before the sync, its own best candidate row for the next column and (its
+// owner) the row at the next diagonal position, double-buffered by column
+// parity; after the sync the winner's candidate row IS the pivot row.  The
+// arithmetic per element is the decoded-domain update of k_leaf_coop, in the
+// same textbook order.
+__device__ __forceinline__ void leaf_publish(const uint32_t* tile, int W, int64_t rb, int nr, int64_t jn,
+                                             unsigned long long best, LeafWs* ws, int par, int tid, int NT) {
+  if (best != 0ull) {
+    const int64_t r = (int64_t)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
+    const int li = (int)(r - rb);
+    for (int c = tid; c < W; c += NT) ws->cand[par][blockIdx.x][c] = tile[li * W + c];
+  }
+  if (jn >= rb && jn < rb + nr)
+    for (int c = tid; c < W; c += NT) ws->jrow[par][c] = tile[(int)(jn - rb) * W + c];
+}
+
+__global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, int64_t m, int64_t w,
+                                                     int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
+                                                     int64_t row_base, LeafWs* ws) {
+  extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long cbest;                // this CTA's best candidate key (next column)
+  __shared__ uint4 urow[64];                          // the pivot row as decoded B operands {M, E, sg, fast}
+  __shared__ uint32_t urowp[64];                      // ... and as patterns
+  __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];      // the MAC's constant tables
+  const int NT = blockDim.x;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  pg::fill_tables(tp, tx, tid, NT);
+  pg::MacConst K;
+  K.one = 1u;
+  K.sixteen = 16u;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(tx + pg::TBIAS) - 30u * 16u;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t re = (rb + rows_per_cta) < m ? (rb + rows_per_cta) : m;
+  const int nr = re > rb ? (int)(re - rb) : 0;
+  const int W = (int)w;
+  for (int e = tid; e < nr * W; e += NT) tile[e] = A[(rb + e / W) * lda + e % W];
+  __syncthreads();
+  {
+    unsigned long long best = 0ull;
+    for (int i = tid; i < nr; i += NT) {
+      const unsigned long long k = piv_key(tile[i * W], rb + i);
+      best = k > best ? k : best;
+    }
+    best = block_max(best, red);
+    if (tid == 0) {
+      cbest = best;
+      if (best != 0ull) atomicMax(&ws->key[0], best);
+    }
+    __syncthreads();
+    leaf_publish(tile, W, rb, nr, 0, cbest, ws, 0, tid, NT);
+  }
+  const int64_t jmax = m < w ? m : w;
+  for (int64_t j = 0; j < jmax; j++) {
+    const int par = (int)(j & 1);
+    grid.sync();
+    const unsigned long long key = __ldcg(&ws->key[j]);
+    const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+    const uint32_t* rowp = ws->cand[par][p / rows_per_cta];
+    const uint32_t* rowj = ws->jrow[par];
+    const uint32_t v = __ldcg(rowp + j);
+    if (blockIdx.x == 0 && tid == 0) {
+      ipiv[j] = (int32_t)(row_base + p + 1);
+      if (v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
+    }
+    const bool swp = v != 0u && p != j;
+    if (swp) {                                        // swap rows j and p (whole leaf width)
+      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = __ldcg(rowp + c);
+      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = __ldcg(rowj + c);
+    }
+    const uint32_t* ursrc = swp ? rowp : rowj;        // the row now at position j
+    for (int c = tid; c < W; c += NT) {
+      LaneVal t;
+      const uint32_t x = __ldcg(ursrc + c);
+      lv_load(t, x);
+      urow[c] = make_uint4(t.a.M, (uint32_t)t.a.E, (uint32_t)t.a.sg, lv_operand(t) ? 1u : 0u);
+      urowp[c] = x;
+    }
+    __syncthreads();
+    const int i0 = (int)((j + 1 > rb ? j + 1 : rb) - rb);
+    if (v != 0u) {                                    // Q8 (one division each); skipped for a zero pivot (Q11)
+      pg::Acc dv;
+      const bool dok = pg::acc_decode(v, dv) && v != 0x80000000u && dv.E <= 37 && dv.E >= -37;
+      const double rcp = dok ? __drcp_rn((double)dv.M) * 4294967296.0 : 0.0;
+      for (int i = i0 + tid; i < nr; i += NT) {
+        const uint32_t x = tile[i * W + (int)j];
+        LaneVal t;
+        lv_load(t, x);
+        bool done = false;
+        if (dok && t.dec) done = pg::acc_div(t.a, dv.M, dv.E, dv.sg, rcp, K);
+        tile[i * W + (int)j] = done ? pg::acc_encode(t.a) : div(x, v);
+      }
+    }
+    __syncthreads();
+    const int wq = W - (int)j - 1;
+    if (wq > 0) {
+      unsigned long long best = 0ull;
+      const uint32_t cnt = nr > i0 ? (uint32_t)(nr - i0) * (uint32_t)wq : 0u;
+      for (uint32_t e = tid; e < cnt; e += NT) {
+        const uint32_t ii = e / (uint32_t)wq;
+        const int i = i0 + (int)ii;
+        const int q = (int)j + 1 + (int)(e - ii * (uint32_t)wq);
+        const uint32_t lp = tile[i * W + (int)j];
+        uint4 ad;
+        const bool af = fast_a(lp, ad);
+        const uint4 ub = urow[q];
+        LaneVal c;
+        lv_load(c, tile[i * W + q]);
+        lv_fms_t(c, lp, af, ad, ub.x, (int32_t)ub.y, (int32_t)ub.z, ub.w != 0u, urowp[q], K);
+        const uint32_t nv = lv_pattern(c);
+        tile[i * W + q] = nv;
+        if (q == (int)j + 1) {
+          const unsigned long long k = piv_key(nv, rb + i);
+          best = k > best ? k : best;
+        }
+      }
+      best = block_max(best, red);
+      if (tid == 0) {
+        cbest = best;
+        if (best != 0ull) atomicMax(&ws->key[j + 1], best);
+      }
+      __syncthreads();
+      if (j + 1 < jmax) leaf_publish(tile, W, rb, nr, j + 1, cbest, ws, par ^ 1, tid, NT);
     }
     __syncthreads();
   }
@@ -303,70 +547,6 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
       }
     }
     __syncthreads();
-  }
-}
-
-// ---- decoded lane values for the in-block kernels -----------------------------
-// A value that lives in a register across many posit updates is kept decoded
-// (the GEMM's accumulator format, csrc/gemm.cuh) so that each update
-// c <- c (-) a (x) b runs the decoded-domain MAC (one rounding for the product,
-// one for the difference, as always) instead of decode -> mul -> encode ->
-// decode -> sub -> encode.  Conservative range guards route any update whose
-// operands or result could leave the MAC's exact range (zero / NaR operands,
-// |E| > 37 operands, |E| > 75 values) to the generic pattern path; both are
-// bit-identical by construction.
-struct LaneVal {
-  pg::Acc a;       // decoded (valid when dec)
-  uint32_t pat;    // pattern (valid when !dec)
-  bool dec;
-};
-
-__device__ __forceinline__ void lv_load(LaneVal& v, uint32_t x) {
-  v.pat = x;
-  v.dec = pg::acc_decode(x, v.a) && (x == 0u || (v.a.E <= 75 && v.a.E >= -75));
-}
-
-__device__ __forceinline__ uint32_t lv_pattern(const LaneVal& v) { return v.dec ? pg::acc_encode(v.a) : v.pat; }
-
-// operand view of a lane value: B format (hidden@30), fast iff nonzero and |E| <= 37
-__device__ __forceinline__ bool lv_operand(const LaneVal& v) {
-  return v.dec && v.a.E > -1000 && v.a.E <= 37 && v.a.E >= -37;
-}
-
-// A-format decode of a pattern operand: fast iff nonzero, not NaR, |E| <= 37
-__device__ __forceinline__ bool fast_a(uint32_t x, uint4& d) {
-  uint32_t sp = 0u;
-  d = pg::stage_decode<31>(x, 0u, sp);
-  return sp == 0u && (int32_t)d.y <= 37 && (int32_t)d.y >= -37;
-}
-
-// c <- c (-) a (x) b; a = pattern (with its A-format decode), b = operand lane
-// value broadcast as (M, E, sg) plus its pattern bp.
-__device__ __forceinline__ void lv_fms(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
-                                       int32_t bsg, bool bfast, uint32_t bp) {
-  if (afast && bfast && c.dec) {
-    uint32_t bad = 0u;
-    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, pg::CalcConst(), bad);
-    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
-    if (!c.dec) c.pat = pg::acc_encode(c.a);                 // |E| in (75, 107]: exact, leave the fast range
-  } else {
-    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
-    lv_load(c, r);
-  }
-}
-
-// lv_fms with the GEMM's shared-memory tables (or any table type)
-template <class Tab>
-__device__ __forceinline__ void lv_fms_t(LaneVal& c, uint32_t ap, bool afast, const uint4& ad, uint32_t bM, int32_t bE,
-                                         int32_t bsg, bool bfast, uint32_t bp, const Tab& K) {
-  if (afast && bfast && c.dec) {
-    uint32_t bad = 0u;
-    pg::mac(c.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bsg, K, bad);
-    c.dec = c.a.E <= 75 && c.a.E >= -75 ? true : (c.a.E < -1000);
-    if (!c.dec) c.pat = pg::acc_encode(c.a);
-  } else {
-    const uint32_t r = sub(lv_pattern(c), mul(ap, bp));
-    lv_load(c, r);
   }
 }
 
@@ -957,7 +1137,7 @@ static int64_t panel_leaf() {
 // update launch that also searches the next column's pivot.
 static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
                       LeafWs* ws, bool allow_coop, cudaStream_t st) {
-  if (cudaMemsetAsync(ws, 0, sizeof(LeafWs), st) != cudaSuccess) return POSIT_ECUDA;
+  if (cudaMemsetAsync(ws, 0, LEAF_WS_ZERO, st) != cudaSuccess) return POSIT_ECUDA;
   // one cooperative launch when the rows fit the CTAs' shared memory
   struct CoopCfg { int coop; int nsm; };
   static const CoopCfg cfg = [] {
@@ -970,6 +1150,7 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
     if (!ok) c.coop = 0;
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_leaf_coop1, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     return c;
   }();
   const int coop = cfg.coop, nsm = cfg.nsm;
@@ -984,7 +1165,9 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
     pb_count_launch();
-    if (cudaLaunchCooperativeKernel((const void*)k_leaf_coop, dim3(grid), dim3(nthr), args, smem, st) == cudaSuccess)
+    // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known)
+    const void* kfn = (coop == 2 || grid > (unsigned)LEAF_MAXCTA) ? (const void*)k_leaf_coop : (const void*)k_leaf_coop1;
+    if (cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthr), args, smem, st) == cudaSuccess)
       return last_launch();
     (void)cudaGetLastError();                          // fall back to the per-column launches
   }
@@ -1080,21 +1263,30 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   if (m <= 0 || n <= 0) return 0;
   if (n <= FR_NMAX) {
     // one fused launch: each CTA solves FR_ROWS whole rows
-    static const int rows = [] {
-      const char* e = getenv("POSIT_RLTN_ROWS");
+    // variant: W lanes per row x FR_ROWS rows per CTA (env POSIT_RLTN = "W,ROWS")
+    static const int var = [] {
+      const char* e = getenv("POSIT_RLTN");
+      int w = 16, r = 16;
+      if (e) sscanf(e, "%d,%d", &w, &r);
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 32>));
-      return e ? atoi(e) : 16;
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<8, 16>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<8, 32>));
+      return w * 100 + r;
     }();
     pb_count_launch();
-    if (rows == 32)
-      k_trsm_rltn_fused<16, 32><<<(unsigned)((m + 31) / 32), 32 * 16, sizeof(FrSmem<16, 32>), st>>>(L, ldl, B, ldb, m,
-                                                                                                   n, stop, 1);
-    else
-      k_trsm_rltn_fused<16, 16><<<(unsigned)((m + 15) / 16), 16 * 16, sizeof(FrSmem<16, 16>), st>>>(L, ldl, B, ldb, m,
-                                                                                                   n, stop, 1);
+#define PB_RLTN(W_, R_)                                                                                              \
+  k_trsm_rltn_fused<W_, R_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(L, ldl, B, ldb, m, \
+                                                                                                   n, stop, 1)
+    if (var == 1632) PB_RLTN(16, 32);
+    else if (var == 816) PB_RLTN(8, 16);
+    else if (var == 832) PB_RLTN(8, 32);
+    else PB_RLTN(16, 16);
+#undef PB_RLTN
     return last_launch();
   }
   for (int64_t j0 = 0; j0 < n; j0 += TBR) {
