@@ -1306,8 +1306,55 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
 // Recursive diagonal-block Cholesky (the traversal of LAPACK potrf2): leaf
 // blocks of <= 32 in shared memory, TRSM + SYRK between them.  Every stage
 // is a no-op once *info != 0.
+// Small SYRK inside the diagonal-block Cholesky: C_lower <- C_lower (-) A A^T
+// with one thread per lower element (ascending k per element, Q6).  For
+// n <= 256 and k = 32 the GEMM kernel would run on a handful of CTAs with long
+// per-thread loops; here every element is its own (short) chain.  A no-op
+// once *stop != 0.
+__global__ void __launch_bounds__(256) k_syrk_tiny(int64_t n, int64_t k, const uint32_t* A, int64_t lda, uint32_t* C,
+                                                   int64_t ldc, const int32_t* stop) {
+  if (stop != nullptr && *stop != 0) return;
+  const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
+  if ((int64_t)blockIdx.x > (int64_t)blockIdx.y || i >= n || j > i) return;
+  LaneVal c;
+  lv_load(c, C[i * ldc + j]);
+  for (int64_t q = 0; q < k; q++) {
+    const uint32_t ap = A[i * lda + q], bp = A[j * lda + q];
+    uint4 ad;
+    const bool af = fast_a(ap, ad);
+    LaneVal bv;
+    lv_load(bv, bp);
+    lv_fms(c, ap, af, ad, bv.a.M, bv.a.E, bv.a.sg, lv_operand(bv), bp);
+  }
+  C[i * ldc + j] = lv_pattern(c);
+}
+
 int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_base, cudaStream_t st) {
   if (b <= 0) return 0;
+  static const int mode = [] {                   // 1: blocked right-looking, 32-wide (default); 0: recursive
+    const char* e = getenv("POSIT_POTF2");
+    return e ? atoi(e) : 1;
+  }();
+  if (mode == 1 && b <= 256) {
+    // right-looking by 32-wide block columns: leaf, the rows below by TRSM,
+    // the trailing lower triangle by the one-thread-per-element SYRK
+    for (int64_t j0 = 0; j0 < b; j0 += TB) {
+      const int64_t jb = (b - j0) < TB ? (b - j0) : TB;
+      uint32_t* Ajj = A + j0 * lda + j0;
+      pb_count_launch();
+      k_potf2_leaf<<<1, 1024, 0, st>>>(Ajj, lda, jb, info, row_base + j0);
+      const int64_t r = b - j0 - jb;
+      if (r > 0) {
+        int rc;
+        if ((rc = pb_trsm_rltn(r, jb, Ajj, lda, Ajj + jb * lda, lda, info, st))) return rc;
+        pb_count_launch();
+        const unsigned t = (unsigned)((r + 15) / 16);
+        k_syrk_tiny<<<dim3(t, t), 256, 0, st>>>(r, jb, Ajj + jb * lda, lda, Ajj + jb * lda + jb, lda, info);
+      }
+    }
+    return last_launch();
+  }
   if (b <= TB) {
     pb_count_launch();
     k_potf2_leaf<<<1, 1024, 0, st>>>(A, lda, b, info, row_base);
