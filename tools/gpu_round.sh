@@ -11,6 +11,8 @@ timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_$TAG.lo
 echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 echo "bench exit $?" >> gpurun_out/bench_$TAG.err
+python bench.py --workload lu --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_lu_$TAG.json 2> gpurun_out/bench_lu_$TAG.err
+python bench.py --workload cholesky --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_chol_$TAG.json 2> gpurun_out/bench_chol_$TAG.err
 timeout 900 python tools/time_lapack.py > gpurun_out/lapack_$TAG.log 2>&1
 if [ "$2" != "skip_ncu" ]; then
 BCMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"

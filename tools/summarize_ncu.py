@@ -90,18 +90,22 @@ def main():
     t_ms = to_ms(*m["gpu__time_duration.sum"])
     lines += ["", f"lane-instructions per MAC (smsp__inst_executed.sum x 32 / MACs): **{ipm:.2f}**",
               f"DRAM traffic per launch: {dram / 1e6:.1f} MB", ""]
-    agg = launches(lcsv)
-    tot = sum(t for _, t in agg.values())
-    with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
-        f.write("kernel,launches,total_ns,share\n")
-        for k, (c, t) in agg.items():
-            f.write(f"\"{k}\",{c},{t:.0f},{t / tot:.4f}\n")
-    lines += ["## launch list (ncu gpu__time_duration.sum, --clock-control none)", "",
-              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
-    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| `{k[:90]}` | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")
+    if lcsv != "-":
+        agg = launches(lcsv)
+        tot = sum(t for _, t in agg.values())
+        with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
+            f.write("kernel,launches,total_ns,share\n")
+            for k, (c, t) in agg.items():
+                f.write(f"\"{k}\",{c},{t:.0f},{t / tot:.4f}\n")
+        lines += ["## launch list (ncu gpu__time_duration.sum, --clock-control none)", "",
+                  "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            lines.append(f"| `{k[:90]}` | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")
     with open(os.path.join(PROF, f"{tag}_gemm_ncu.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
+    if lcsv == "-":                     # a side capture (e.g. the C4 trailing shape): not the bench's profile
+        print("\n".join(lines))
+        return
     prof = {"tag": tag, "kernel": name, "inst_per_mac": ipm, "dram_bytes_per_launch": dram, "ncu_time_ms": t_ms,
             "alu_pipe_pct": float(m["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"][0]),
             "fma_pipe_pct": float(m["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"][0]),
