@@ -34,6 +34,25 @@ namespace pg {
 #ifndef PG_AD_SAD
 #define PG_AD_SAD 0
 #endif
+#ifndef PG_SIGN_LOP             // sign products as LOP3 (ALU) instead of IMAD (FMA-heavy)
+#define PG_SIGN_LOP 0
+#endif
+// Ex + 30 and |Ep - Ec| as plain adds (ptxas emits IMAD.IADD / IADD3) instead
+// of IMADs with a register multiplier: C2 1149 -> 1173 Gflop/s on one box
+// (r03f/r03g A/B; moving the sign products or the zero-flag offset to the ALU
+// instead, or the table addresses to LEA, is slower)
+#ifndef PG_EXI_ALU
+#define PG_EXI_ALU 1
+#endif
+#ifndef PG_AD_ALU
+#define PG_AD_ALU 1
+#endif
+#ifndef PG_TAB_ADDR_PLAIN       // table addresses as plain index * 16 + base (ptxas picks the pipe)
+#define PG_TAB_ADDR_PLAIN 0
+#endif
+#ifndef PG_CE_ALU                // zero-flag scale offset by shift / and instead of IMAD
+#define PG_CE_ALU 0
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -158,9 +177,25 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 struct MacConst {
   uint32_t one, sixteen;               // = 1, 16 at run time (opaque to ptxas)
   uint32_t tp0, tx0;                   // shared-memory byte addresses of table entry E = 0 (tx: Ex + 30 = 0)
+#if PG_TAB_ADDR_PLAIN == 2
+  // IMAD with an immediate multiplier (two register reads instead of three)
+  static __device__ __forceinline__ uint32_t addr16(uint32_t i, uint32_t base) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, 16, %2;" : "=r"(d) : "r"(i), "r"(base));
+    return d;
+  }
+  __device__ __forceinline__ uint4 prod(int32_t Ep) const { return lds128(addr16((uint32_t)Ep, tp0)); }
+  __device__ __forceinline__ uint4 prod2(int32_t S) const { return lds128(addr16((uint32_t)S, tp0)); }
+  __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(addr16(Exi, tx0)); }
+#elif PG_TAB_ADDR_PLAIN
+  __device__ __forceinline__ uint4 prod(int32_t Ep) const { return lds128((uint32_t)Ep * 16u + tp0); }
+  __device__ __forceinline__ uint4 prod2(int32_t S) const { return lds128((uint32_t)S * 16u + tp0); }
+  __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(Exi * 16u + tx0); }
+#else
   __device__ __forceinline__ uint4 prod(int32_t Ep) const { return lds128(fmad((uint32_t)Ep, sixteen, tp0)); }
   __device__ __forceinline__ uint4 prod2(int32_t S) const { return lds128(fmad((uint32_t)S, sixteen, tp0)); }
   __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(fmad(Exi, sixteen, tx0)); }
+#endif
 };
 
 // The same constants computed in registers (no shared-memory tables): used by
@@ -224,7 +259,11 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
       "addc.u32 %0, %3, 0;\n\t}"
       : "=r"(rp) : "r"(lo), "r"(yp | (qp & 1u)), "r"(qp));
   const uint32_t Mp = fmad(rp, mulp, 0u);             // hidden@30 (2^31 if rounding carried)
+#if PG_SIGN_LOP
+  const int32_t sp = (sa ^ sb) | 1;                   // +-1 x +-1 as one LOP3: (-1 = ~0, 1 = 1)
+#else
   const int32_t sp = (int32_t)fmad((uint32_t)sa, (uint32_t)sb, 0u);
+#endif
 
   // -- sum: exact aligned add with jammed sticky, rounded once at f_s(Ex) --
   // lexicographic (E, M) compare as one 64-bit signed compare: branch-free
@@ -237,6 +276,8 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   const int32_t Ebg = max(Ep, c.E);
 #if PG_AD_SAD
   const uint32_t ad = __sad(Ep, c.E, 0u);                      // |Ep - Ec| in one ALU op (FMA pipe is the busier)
+#elif PG_AD_ALU
+  const uint32_t ad = (uint32_t)(Ebg + Ebg - Ep - c.E);        // |Ep - Ec| = 2 max - Ep - Ec
 #else
   const uint32_t ad = fmad((uint32_t)Ebg, 2u * K.one, 0u - fmad((uint32_t)Ep, K.one, (uint32_t)c.E));  // |Ep - Ec|
 #endif
@@ -244,12 +285,20 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   const uint32_t lost = __funnelshift_rc(0u, Msm, ad);        // bits shifted out (nonzero iff any)
   uint32_t jam;
   asm("min.u32 %0, %1, 1;" : "=r"(jam) : "r"(lost));          // sticky of the shifted-out bits
+#if PG_SIGN_LOP
+  const uint32_t sgn = (uint32_t)((sp ^ c.sg) | 1);              // +1 add, -1 subtract
+#else
   const uint32_t sgn = fmad((uint32_t)sp, (uint32_t)c.sg, 0u);   // +1 add, -1 subtract
+#endif
   const uint32_t x = fmad(sh | jam, sgn, Mbg);                // |big| +/- |small|, >= 0
   uint32_t flo;
   asm("bfind.u32 %0, %1;" : "=r"(flo) : "r"(x));             // leading one (0xFFFFFFFF if x == 0)
   const uint32_t xf = __funnelshift_r(0u, x, flo);            // fraction bits left-aligned (hidden dropped)
+#if PG_EXI_ALU
+  const uint32_t Exi = flo + (uint32_t)Ebg;                   // Ex + 30
+#else
   const uint32_t Exi = fmad(flo, K.one, (uint32_t)Ebg);       // Ex + 30
+#endif
   const uint4 U = K.sum(Exi);
   uint32_t qx, yx;
   mulwide(xf, U.x, qx, yx);                                   // f_s fraction bits | the rest, left-aligned
@@ -263,7 +312,11 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   c.M = Mn >> cy;
   // exact cancellation (x == 0, flo = -1): scale pushed far below any product,
   // so the (zero) accumulator is the small operand of every later add
+#if PG_CE_ALU
+  c.E = (int32_t)(U.w + cy) + (((int32_t)flo >> 31) & -4096);
+#else
   c.E = (int32_t)fmad((uint32_t)((int32_t)flo >> 31), 4096u, U.w + cy);
+#endif
   c.sg = sbg;
   if (TRACK) badacc = fmad(U.z, K.one, badacc);               // BAD_FLAG bits accumulate
 }
