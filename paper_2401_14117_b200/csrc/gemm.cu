@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (!TRANS_B) {
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30>(rb[h * 4 + q], flip, sp);
+        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30>(rb[h * 4 + q], flip, sp, K.tp0);
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30>(rb[h * 4 + q], flip, sp);
+        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30>(rb[h * 4 + q], flip, sp, K.tp0);
       }
     }
     return sp;
@@ -291,14 +291,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         const int64_t av = P.n - (col0 + bc);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk][bc + q] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp);
+          S.b[buf][bk][bc + q] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
         const bool rok = col0 + bc < P.n;
         const int64_t av = P.k - (k0 + bk);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk + q][bc] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp);
+          S.b[buf][bk + q][bc] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
       }
     }
     return sp;
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y,
-                                   (int32_t)bv[j].z, K, badacc);
+              mac<MacConst, false, PG_PRESCALED != 0>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+                                                      (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x, (int32_t)bv[j].y,
-                                   (int32_t)bv[j].z, K, badacc);
+              mac<MacConst, false, PG_PRESCALED != 0>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+                                                      (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       }
     } else if (!bad) {

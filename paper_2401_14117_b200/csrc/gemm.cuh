@@ -53,6 +53,9 @@ namespace pg {
 #ifndef PG_CE_ALU                // zero-flag scale offset by shift / and instead of IMAD
 #define PG_CE_ALU 0
 #endif
+#ifndef PG_PRESCALED             // product table address = Aw + Bw (staged 16 E [+ base]) instead of an IMAD:
+#define PG_PRESCALED 0           // one instruction fewer per MAC but an ALU add (C2 1167 vs 1173, r03i) -> off
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -78,7 +81,7 @@ struct Params {
 // Staged element = {M, E, sigma (+1 / -1 as int), 0}.  Returns "special"
 // (zero, NaR, |E| > 53) through `special`.
 template <int HID>
-__device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_t& special) {
+__device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_t& special, uint32_t wbase = 0u) {
   const uint32_t s = (x >> 31) ^ flip;
   const uint32_t a = (x >> 31) ? (0u - x) : x;
   const uint32_t y = a << 1;
@@ -89,7 +92,8 @@ __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_
   const int E = 4 * k + (int)(rest >> 30);
   const uint32_t M = (0x80000000u | ((rest << 2) >> 1)) >> (31 - HID);
   special |= (uint32_t)((x << 1) == 0u) | (uint32_t)(E > E_STAGE_MAX) | (uint32_t)(E < -E_STAGE_MAX);
-  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, 0u);
+  // .w: 16 E + wbase, so that a product's table address is one add of the two operands' .w (PG_PRESCALED)
+  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, (uint32_t)E * 16u + wbase);
 }
 
 // ---- accumulator <-> pattern (exact: the accumulator is on the lattice) ----
@@ -232,16 +236,16 @@ struct CalcConst {
 // The GEMM does not track per MAC: with |Ea|, |Eb| <= 37 (staging) and
 // |Ec| <= 91 at the slab start, |Ep| <= 75, a sum's scale grows by at most 1
 // per MAC (<= 107 after 16) and cancellation stops at Ebg - 31 >= -106.
-template <class Tab, bool TRACK = true>
+template <class Tab, bool TRACK = true, bool PRE = false>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
-                                    const Tab& K, uint32_t& badacc) {
+                                    const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
   uint32_t hi, lo;
   mulwide(Ma, Mb, hi, lo);                            // hi in [2^29, 2^31)
   const uint32_t n = hi >> 30;
 #if PG_PROD_BY_SUM
   // the table lookup depends only on Ea + Eb, so it overlaps the multiply
-  const uint4 T = K.prod2(Ea + Eb);
+  const uint4 T = PRE ? lds128(aw + bw) : K.prod2(Ea + Eb);
   const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
   const uint32_t mulp = fmad(n, T.w, T.z);
 #else
