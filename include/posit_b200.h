@@ -108,7 +108,11 @@ int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, 
 /* HOST variant of posit_gemm (end-to-end path): A, B, C are HOST arrays
  * (pinned memory recommended); `dwork` is a DEVICE workspace of at least
  * posit_gemm_host_work_bytes(m, n, k) bytes.  Copies A, B, C to the device,
- * runs posit_gemm, copies C back and synchronises `stream`. */
+ * runs posit_gemm, copies C back and synchronises `stream`.  With transa = 'N'
+ * and m >= 1024 the work is pipelined in row chunks of C (internal streams and
+ * events; B first, then each chunk's A and C rows up while the previous chunk
+ * computes and the one before comes back); the result is bit-identical (row
+ * chunks are independent outputs, Q6).  Returns after the copies complete. */
 size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k);
 int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
                     const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,

@@ -118,6 +118,93 @@ size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k) {
   return (size_t)4 * (size_t)(m * k + k * n + m * n) + 256;
 }
 
+// Pipelined host GEMM (transa = 'N'): C's rows in chunks; chunk i's A rows
+// and C rows go up on a copy stream while chunk i-1 computes (two compute
+// streams, so one chunk's last wave overlaps the next chunk's first) and chunk
+// i-2's C comes back on a third stream.  B goes up first, once.  Row chunks
+// are independent outputs with unchanged per-element order, so the bits equal
+// the one-launch GEMM.  POSIT_HOST_PIPELINE=0 forces the serial schedule.
+static constexpr int64_t HOST_CHUNK_MIN = 512;
+static int host_pipeline_env() {
+  static const int v = [] {
+    const char* e = getenv("POSIT_HOST_PIPELINE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+static int gemm_host_pipelined(char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
+                               int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
+                               uint32_t* dA, uint32_t* dB, uint32_t* dC, cudaStream_t st) {
+  const int64_t brow = transb == 'N' ? k : n, bcol = transb == 'N' ? n : k;
+  int64_t nch = m / HOST_CHUNK_MIN;
+  if (nch > 8) nch = 8;
+  const int64_t rows = (((m + nch - 1) / nch) + 63) / 64 * 64;
+  nch = (m + rows - 1) / rows;
+  constexpr int MAXCH = 8;
+  cudaStream_t cs = nullptr, ds = nullptr, ks[2] = {nullptr, nullptr};
+  cudaEvent_t ev0 = nullptr, ev_in[MAXCH] = {}, ev_done[MAXCH] = {}, ev_end = nullptr;
+  int rc = 0;
+  auto cleanup = [&]() {
+    for (int i = 0; i < MAXCH; i++) {
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev_end) cudaEventDestroy(ev_end);
+    if (cs) cudaStreamDestroy(cs);
+    if (ds) cudaStreamDestroy(ds);
+    for (auto& q : ks)
+      if (q) cudaStreamDestroy(q);
+  };
+  auto ck = [&](cudaError_t e) { if (e != cudaSuccess && rc == 0) rc = cuda_check(e); return rc == 0; };
+  if (!ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) || !ck(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking)) ||
+      !ck(cudaStreamCreateWithFlags(&ks[0], cudaStreamNonBlocking)) ||
+      !ck(cudaStreamCreateWithFlags(&ks[1], cudaStreamNonBlocking)) ||
+      !ck(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming)) ||
+      !ck(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming))) {
+    cleanup();
+    return rc;
+  }
+  for (int i = 0; i < nch; i++)
+    if (!ck(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming)) ||
+        !ck(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming))) {
+      cleanup();
+      return rc;
+    }
+  // everything after the caller's earlier work on st
+  ck(cudaEventRecord(ev0, st));
+  for (cudaStream_t q : {cs, ds, ks[0], ks[1]}) ck(cudaStreamWaitEvent(q, ev0, 0));
+  ck(cudaMemcpy2DAsync(dB, (size_t)bcol * 4, B, (size_t)ldb * 4, (size_t)bcol * 4, (size_t)brow, cudaMemcpyHostToDevice,
+                       cs));
+  for (int64_t i = 0; i < nch && rc == 0; i++) {
+    const int64_t r0 = i * rows, mr = (m - r0) < rows ? (m - r0) : rows;
+    ck(cudaMemcpy2DAsync(dA + r0 * k, (size_t)k * 4, A + r0 * lda, (size_t)lda * 4, (size_t)k * 4, (size_t)mr,
+                         cudaMemcpyHostToDevice, cs));
+    if (beta != 0u)
+      ck(cudaMemcpy2DAsync(dC + r0 * n, (size_t)n * 4, C + r0 * ldc, (size_t)ldc * 4, (size_t)n * 4, (size_t)mr,
+                           cudaMemcpyHostToDevice, cs));
+    ck(cudaEventRecord(ev_in[i], cs));
+    cudaStream_t q = ks[i & 1];
+    ck(cudaStreamWaitEvent(q, ev_in[i], 0));
+    if (rc == 0) {
+      const int g = posit_gemm('N', transb, mr, n, k, alpha, dA + r0 * k, k > 0 ? k : 1, dB, bcol > 0 ? bcol : 1, beta,
+                               dC + r0 * n, n > 0 ? n : 1, q);
+      if (g) rc = g;
+    }
+    ck(cudaEventRecord(ev_done[i], q));
+    ck(cudaStreamWaitEvent(ds, ev_done[i], 0));
+    ck(cudaMemcpy2DAsync(C + r0 * ldc, (size_t)ldc * 4, dC + r0 * n, (size_t)n * 4, (size_t)n * 4, (size_t)mr,
+                         cudaMemcpyDeviceToHost, ds));
+  }
+  ck(cudaEventRecord(ev_end, ds));
+  ck(cudaStreamWaitEvent(st, ev_end, 0));
+  if (rc == 0) ck(cudaStreamSynchronize(st));
+  else cudaStreamSynchronize(ds);
+  cleanup();
+  return rc;
+}
+
 int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha, const uint32_t* A,
                     int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
                     void* dwork, size_t work_bytes, void* stream) {
@@ -134,6 +221,8 @@ int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, u
   uint32_t* dC = dB + k * n;
   cudaStream_t st = S(stream);
   int rc;
+  if (transa == 'N' && k > 0 && m >= 2 * HOST_CHUNK_MIN && host_pipeline_env())
+    return gemm_host_pipelined(transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, dA, dB, dC, st);
   if ((rc = cuda_check(cudaMemcpy2DAsync(dA, (size_t)acol * 4, A, (size_t)lda * 4, (size_t)acol * 4, (size_t)arow,
                                          cudaMemcpyHostToDevice, st))))
     return rc;

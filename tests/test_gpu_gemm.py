@@ -162,3 +162,28 @@ def test_gemm_eq2_general_alpha_beta(cuda_ok, transa, transb, alpha, beta):
     dC = to_dev(C)
     PB.posit_gemm_eq2(to_dev(A), to_dev(B), dC, a, b, transb=transb, transa=transa)
     assert mismatch(to_host(dC), O.gemm_eq2(A, B, C, a, b, transa=transa, transb=transb)) == 0
+
+
+@pytest.mark.parametrize("transb", ["N", "T"])
+@pytest.mark.parametrize("beta", [ONE, 0])
+def test_gemm_host_pipelined_matches_oracle(cuda_ok, transb, beta):
+    # posit_gemm_host with m >= 1024 takes the chunked, stream-pipelined schedule
+    # (two row chunks here: 576 rows and a ragged 524); sampled rows around the
+    # chunk boundary are checked against the oracle, all of C against the device GEMM.
+    import os
+    import torch
+    import paper_2401_14117_b200 as PB
+    m, n, k = 1100, 96, 70
+    A64, B64, C64 = SI.config2(n=n, m=m, k=k)
+    if transb == "T":
+        B64 = B64.T.copy()
+    A, B, C = _pats(A64), _pats(B64), _pats(C64)
+    h = [torch.from_numpy(x.view(np.int32)).pin_memory() for x in (A, B, C)]
+    dwork = torch.empty(PB.posit_gemm_host_work_bytes(m, n, k), dtype=torch.uint8, device="cuda")
+    PB.posit_gemm_host(h[0], h[1], h[2], dwork, transb=transb, beta=beta)
+    got = h[2].numpy().view(np.uint32).copy()
+    rows = np.r_[0:3, 570:582, 1090:1100]
+    ref = O.gemm(A[rows], B, C[rows] if beta else np.zeros_like(C[rows]), transb=transb, beta=beta)
+    assert mismatch(got[rows], ref) == 0
+    dev = _gpu_gemm(A, B, C, transb=transb, beta=beta)
+    assert mismatch(got, dev) == 0
