@@ -481,6 +481,12 @@ double model_time(int64_t m, int64_t n, bool syrk) {
 // bits (same per-element order), so the choice is performance only.
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   if (P.m == 0 || P.n == 0) return 0;
+  // tiny shapes (the panel-internal updates): one thread per output
+  static const int tiny_env = [] {
+    const char* e = getenv("POSIT_GEMM_TINY");
+    return e ? atoi(e) : 1;
+  }();
+  if (tiny_env && P.k >= 1 && P.k <= 64 && P.m <= 128 && P.n <= 128) return pb_launch_gemm_tiny(P, transb, syrk, st);
   int v = variant();
   if (v == 0) {
     const double w2 = model_time<V2>(P.m, P.n, syrk), w1 = model_time<V1>(P.m, P.n, syrk);

@@ -10,6 +10,7 @@ namespace pg { struct Params; }
 
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
 int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
+int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);   // lapack.cu
 
 // lapack.cu
 int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,

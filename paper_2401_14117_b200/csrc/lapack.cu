@@ -1306,6 +1306,53 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
 // Recursive diagonal-block Cholesky (the traversal of LAPACK potrf2): leaf
 // blocks of <= 32 in shared memory, TRSM + SYRK between them.  Every stage
 // is a no-op once *info != 0.
+// Tiny GEMM / SYRK (the panel-internal updates: m, n <= 128, K <= 64): one
+// thread per output element, its chain of K updates in ascending k (Q6), each
+// the decoded-domain MAC with the generic fallback.  A single-CTA launch of the
+// tiled kernel spends ~56 us on such a shape (long per-thread loops on one SM);
+// this one is bound by one short chain.  alpha = +1 adds: b enters negated
+// (exact).  SYRK: lower triangle only.  A no-op once *stop != 0.
+__global__ void __launch_bounds__(256) k_gemm_tiny(pg::Params P, int transb, int syrk) {
+  if (P.stop != nullptr && *P.stop != 0) return;
+  const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
+  if (i >= P.m || j >= P.n || (syrk && j > i)) return;
+  LaneVal c;
+  lv_load(c, P.beta ? P.C[i * P.ldc + j] : 0u);
+  // operands in chunks of 8, all loads of a chunk in flight before its chain
+  constexpr int CH = 8;
+  const int64_t sa = P.transa ? P.lda : 1, sa0 = P.transa ? i : i * P.lda;
+  const int64_t sb = transb ? 1 : P.ldb, sb0 = transb ? j * P.ldb : j;
+  for (int64_t q0 = 0; q0 < P.k; q0 += CH) {
+    uint32_t a[CH], b[CH];
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const bool in = q0 + u < P.k;
+      a[u] = in ? P.A[sa0 + (q0 + u) * sa] : 0u;
+      b[u] = in ? P.B[sb0 + (q0 + u) * sb] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      if (q0 + u < P.k) {
+        const uint32_t bp = P.neg ? b[u] : 0u - b[u];   // c (+) a b = c (-) a (-b), negation exact
+        uint4 ad;
+        const bool af = fast_a(a[u], ad);
+        LaneVal bv;
+        lv_load(bv, bp);
+        lv_fms(c, a[u], af, ad, bv.a.M, bv.a.E, bv.a.sg, lv_operand(bv), bp);
+      }
+    }
+  }
+  P.C[i * P.ldc + j] = lv_pattern(c);
+}
+
+int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+  pb_count_launch();
+  const dim3 grid((unsigned)((P.n + 15) / 16), (unsigned)((P.m + 15) / 16));
+  k_gemm_tiny<<<grid, 256, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
+  return last_launch();
+}
+
 // Small SYRK inside the diagonal-block Cholesky: C_lower <- C_lower (-) A A^T
 // with one thread per lower element (ascending k per element, Q6).  For
 // n <= 256 and k = 32 the GEMM kernel would run on a handful of CTAs with long

@@ -187,3 +187,27 @@ def test_gemm_host_pipelined_matches_oracle(cuda_ok, transb, beta):
     assert mismatch(got[rows], ref) == 0
     dev = _gpu_gemm(A, B, C, transb=transb, beta=beta)
     assert mismatch(got, dev) == 0
+
+
+@pytest.mark.parametrize("transa", ["N", "T"])
+@pytest.mark.parametrize("transb", ["N", "T"])
+@pytest.mark.parametrize("alpha,beta", [(MONE, ONE), (ONE, 0)])
+def test_gemm_tiny_path_special_values(cuda_ok, transa, transb, alpha, beta):
+    # m, n <= 128 and K <= 64 run the one-thread-per-output kernel (the panel-
+    # internal updates); zeros, NaR, extreme scales and accumulators beyond the
+    # fast range force its generic fallback on some elements
+    m, n, k = 60, 100, 40
+    A = _pats(SI.normal_matrix((m, k), 1.0, 21))
+    B = _pats(SI.normal_matrix((k, n), 1e3, 22))
+    C = _pats(SI.normal_matrix((m, n), 1e20, 23))
+    A[5, 7] = O.P32_NAR
+    A[9, :] = 0
+    A[11, 3] = O.from_f64(1e30)
+    B[12, 40] = O.from_f64(1e-33)
+    C[:, 0] = O.from_f64(2.0 ** 110)
+    if transa == "T":
+        A = A.T.copy()
+    if transb == "T":
+        B = B.T.copy()
+    ref = O.gemm(A, B, C, transa=transa, transb=transb, alpha=alpha, beta=beta)
+    assert mismatch(_gpu_gemm(A, B, C, transb, alpha=alpha, beta=beta, transa=transa), ref) == 0
