@@ -587,6 +587,44 @@ __global__ void __launch_bounds__(1024) k_trsm_llnu_blk(const uint32_t* L, int64
   if (wid < ib && c0 + lane < n) B[(i0 + wid) * ldb + c0 + lane] = sb[wid][lane];
 }
 
+// The same, NW columns (warps) per CTA and L's block staged decoded: for
+// narrow right-hand sides (the panel-internal TRSMs) the 32-column CTA puts all
+// the (issue-bound) steps on one SM; 8-column CTAs spread them.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_trsm_llnu_blkw(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                           int64_t i0, int64_t ib, int64_t n) {
+  __shared__ uint32_t sb[TB][NW + 1];
+  __shared__ uint4 sld[TB][TB];           // L[i0 + r][i0 + c] decoded A-format {M, E, sigma (0: slow), pattern}
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * NW;
+  for (int r = wid; r < ib; r += NW) {
+    const uint32_t x = lane < r ? L[(i0 + r) * ldl + i0 + lane] : 0u;
+    uint4 d;
+    const bool f = fast_a(x, d);
+    sld[r][lane] = make_uint4(d.x, d.y, f ? d.z : 0u, x);
+    if (lane < NW) sb[r][lane] = (c0 + lane < n) ? B[(i0 + r) * ldb + c0 + lane] : 0u;
+  }
+  __syncthreads();
+  LaneVal b;
+  lv_load(b, lane < ib ? sb[lane][wid] : 0u);
+  for (int k = 0; k < ib - 1; k++) {
+    const bool bf = lv_operand(b);
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, k);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, k);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, k);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, k) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, lane == k ? lv_pattern(b) : 0u, k);   // for the generic path
+    if (lane > k && lane < ib) {
+      const uint4 ad = sld[lane][k];
+      lv_fms(b, ad.w, ad.z != 0u, ad, bM, bE, bs, bfk, bpk);
+    }
+  }
+  if (lane < ib) sb[lane][wid] = lv_pattern(b);
+  __syncthreads();
+  for (int r = wid; r < ib; r += NW)
+    if (lane < NW && c0 + lane < n) B[(i0 + r) * ldb + c0 + lane] = sb[r][lane];
+}
+
 // The same in-block solve with one thread per column of B (default).  Columns
 // are independent, so a thread runs its column's substitution alone: rows in
 // groups of LC_G, each group first taking the updates from every earlier
@@ -1237,6 +1275,10 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
     return v == 0 || v == 4 || v == 8 ? v : -1;
   }();
   const int use_col = col_env >= 0 ? col_env : (n > 148 * TB ? 4 : 0);
+  static const int blk_env = [] {                 // warp-per-column CTA width: 8 (default) or 32 columns
+    const char* e = getenv("POSIT_LLNU_BLK");
+    return e ? atoi(e) : 8;
+  }();
   for (int64_t i0 = 0; i0 < m; i0 += TB) {
     const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
     if (ib > 1) {
@@ -1245,6 +1287,8 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
         k_trsm_llnu_col<8><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
       else if (use_col == 4)
         k_trsm_llnu_col<4><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
+      else if (blk_env == 8)
+        k_trsm_llnu_blkw<8><<<(unsigned)((n + 7) / 8), 256, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
       else
         k_trsm_llnu_blk<<<(unsigned)((n + TB - 1) / TB), 1024, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
     }
