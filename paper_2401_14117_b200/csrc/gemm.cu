@@ -487,6 +487,9 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st)
     return e ? atoi(e) : 1;
   }();
   if (tiny_env && P.k >= 1 && P.k <= 64 && P.m <= 128 && P.n <= 128) return pb_launch_gemm_tiny(P, transb, syrk, st);
+  // tall and skinny with a short K (the panel recursion's innermost updates, m x 32 x 32): a 64-column tile
+  // would idle half its threads on one row of CTAs
+  if (tiny_env == 2 && P.k >= 1 && P.k <= 32 && P.n <= 32 && !syrk) return pb_launch_gemm_tiny(P, transb, syrk, st);
   int v = variant();
   if (v == 0) {
     const double w2 = model_time<V2>(P.m, P.n, syrk), w1 = model_time<V1>(P.m, P.n, syrk);
