@@ -499,6 +499,7 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
   uint32_t (*val)[SWP_COLS] = reinterpret_cast<uint32_t (*)[SWP_COLS]>(swp_smem);   // [2 * SWP_MAX][SWP_COLS]
   __shared__ int32_t tgt[SWP_MAX];      // pivot row of swap s (relative row index)
   __shared__ int16_t slot[SWP_MAX];     // slot holding that row
+  __shared__ int16_t perm[2 * SWP_MAX]; // after the swaps, slot q holds the row gathered into slot perm[q]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * SWP_COLS + lane;
   for (int64_t s0 = k1; s0 < k2; s0 += SWP_MAX) {
@@ -521,29 +522,49 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
       slot[s] = (int16_t)sl;
     }
     __syncthreads();
-    // gather
-    for (int s = wid; s < ns; s += nw) {
-      val[s][lane] = c < ncols ? A[(s0 + s) * lda + c] : 0u;
-      if (slot[s] == ns + s) val[ns + s][lane] = c < ncols ? A[(int64_t)tgt[s] * lda + c] : 0u;
-    }
-    __syncthreads();
-    // swaps in order (warp 0, lane = column)
+    // gather (warps 1..): each warp has up to 8 row segments in flight; meanwhile
+    // warp 0 composes the swaps on slot indices: slot q ends up holding the row
+    // gathered into slot perm[q] (no data moves in the sequential part)
     if (wid == 0) {
-      for (int s = 0; s < ns; s++) {
-        const int q = slot[s];
-        if (q != s) {
-          const uint32_t t = val[s][lane];
-          val[s][lane] = val[q][lane];
-          val[q][lane] = t;
+      for (int q = lane; q < 2 * ns; q += 32) perm[q] = (int16_t)q;
+      __syncwarp();
+      if (lane == 0) {
+        for (int s = 0; s < ns; s++) {
+          const int q = slot[s];
+          if (q != s) {
+            const int16_t t = perm[s];
+            perm[s] = perm[q];
+            perm[q] = t;
+          }
+        }
+      }
+    } else {
+      const int nwg = nw - 1, w = wid - 1;
+      for (int sb = w * 8; sb < ns; sb += nwg * 8) {
+        uint32_t v0[8], v1[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int s = sb + u;
+          const bool in = s < ns && c < ncols;
+          v0[u] = in ? A[(s0 + s) * lda + c] : 0u;
+          v1[u] = (in && slot[s] == ns + s) ? A[(int64_t)tgt[s] * lda + c] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int s = sb + u;
+          if (s < ns) {
+            val[s][lane] = v0[u];
+            if (slot[s] == ns + s) val[ns + s][lane] = v1[u];
+          }
         }
       }
     }
     __syncthreads();
-    // scatter
+    // scatter: position slot q receives slot perm[q]
     for (int s = wid; s < ns; s += nw) {
       if (c < ncols) {
-        A[(s0 + s) * lda + c] = val[s][lane];
-        if (slot[s] == ns + s) A[(int64_t)tgt[s] * lda + c] = val[ns + s][lane];
+        A[(s0 + s) * lda + c] = val[perm[s]][lane];
+        if (slot[s] == ns + s) A[(int64_t)tgt[s] * lda + c] = val[perm[ns + s]][lane];
       }
     }
     __syncthreads();
