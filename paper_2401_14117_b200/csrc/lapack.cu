@@ -1215,8 +1215,13 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
   const int coop = cfg.coop, nsm = cfg.nsm;
   // on the caller's stream: one CTA of 256 threads per SM; on a side stream
   // (lookahead, sharing the SMs with the trailing GEMM): a few CTAs of 1024
-  const int nctas = allow_coop ? nsm : (nsm < 16 ? nsm : 16);
-  const int nthr = allow_coop ? COOP_THREADS : 1024;
+  static const int force = [] {                 // POSIT_LEAF_CTAS = 16 / 148: force one configuration (tests, sweeps)
+    const char* e = getenv("POSIT_LEAF_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const bool wide = force ? force > 16 : allow_coop;
+  const int nctas = wide ? nsm : (nsm < 16 ? nsm : 16);
+  const int nthr = wide ? COOP_THREADS : 1024;
   const int64_t rpc = (m + nctas - 1) / nctas;
   const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
   if (coop && smem <= 160 * 1024 && w <= 64) {
