@@ -325,6 +325,14 @@ static int lookahead_env() {
   return v;
 }
 
+static int64_t wide_leaf_cols() {
+  static const int64_t v = [] {
+    const char* e = getenv("POSIT_WIDE_LEAF_COLS");
+    return e ? (int64_t)atoll(e) : (int64_t)4096;
+  }();
+  return v;
+}
+
 struct SideStream {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_col = nullptr, ev_panel = nullptr;
@@ -384,7 +392,13 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
           // ... then factor it on the side stream while the rest of the update runs
           if ((rc = cuda_check(cudaEventRecord(ss.ev_col, st)))) return rc;
           if ((rc = cuda_check(cudaStreamWaitEvent(ss.side, ss.ev_col, 0)))) return rc;
-          if ((rc = pb_getrf_panel(m - s1, b1, A + s1 * lda + s1, lda, ipiv + s1, info, s1, work, false, ss.side)))
+          // the leaf takes a few SMs while the trailing update is large, every SM
+          // once it is small (the panel is then the critical path: panel_sweep
+          // r03s, m = 2048: 2.6 ms on 16 CTAs vs 2.1 ms on 148; threshold swept in r03u:
+          // C5 376.5 -> 371.0 ms, C4 2618 -> 2613 ms)
+          const bool wide_leaf = (n - s1 - b1) <= wide_leaf_cols();
+          if ((rc = pb_getrf_panel(m - s1, b1, A + s1 * lda + s1, lda, ipiv + s1, info, s1, work, wide_leaf,
+                                   ss.side)))
             return launch_check(rc);
           if ((rc = cuda_check(cudaEventRecord(ss.ev_panel, ss.side)))) return rc;
         }
