@@ -479,6 +479,14 @@ double model_time(int64_t m, int64_t n, bool syrk) {
 // Picks the tile shape with the smallest modelled time for this problem;
 // near-ties (within 10%) go to the 64 x 128 tile.  All configurations compute the same
 // bits (same per-element order), so the choice is performance only.
+static int64_t tiny_outputs() {
+  static const int64_t v = [] {
+    const char* e = getenv("POSIT_TINY_OUTPUTS");
+    return e ? (int64_t)atoll(e) : (int64_t)65536;
+  }();
+  return v;
+}
+
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   if (P.m == 0 || P.n == 0) return 0;
   // tiny shapes (the panel-internal updates): one thread per output
@@ -487,6 +495,9 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st)
     return e ? atoi(e) : 1;
   }();
   if (tiny_env && P.k >= 1 && P.k <= 64 && P.m <= 128 && P.n <= 128) return pb_launch_gemm_tiny(P, transb, syrk, st);
+  // few outputs and a short K (the panel recursion at small heights): the tiled kernel would run a few
+  // CTAs with long per-thread loops (480 x 32 x 32: 54 us), one chain per output is shorter
+  if (tiny_env && P.k >= 1 && P.k <= 128 && P.m * P.n <= tiny_outputs()) return pb_launch_gemm_tiny(P, transb, syrk, st);
   // tall and skinny with a short K (the panel recursion's innermost updates, m x 32 x 32): a 64-column tile
   // would idle half its threads on one row of CTAs
   if (tiny_env == 2 && P.k >= 1 && P.k <= 32 && P.n <= 32 && !syrk) return pb_launch_gemm_tiny(P, transb, syrk, st);

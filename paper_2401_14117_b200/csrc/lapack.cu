@@ -1220,8 +1220,9 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     return e ? atoi(e) : 0;
   }();
   const bool wide = force ? force > 16 : allow_coop;
-  const int nctas = wide ? nsm : (nsm < 16 ? nsm : 16);
-  const int nthr = wide ? COOP_THREADS : 1024;
+  int nctas = wide ? nsm : (nsm < 16 ? nsm : 16);
+  int nthr = wide ? COOP_THREADS : 1024;
+  if (force > 0 && force != 16 && force != 148) { nctas = force < nsm ? force : nsm; nthr = COOP_THREADS; }
   const int64_t rpc = (m + nctas - 1) / nctas;
   const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
   if (coop && smem <= 160 * 1024 && w <= 64) {

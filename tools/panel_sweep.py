@@ -13,7 +13,7 @@ import paper_2401_14117_b200 as PB  # noqa: E402
 import synthetic_inputs as SI  # noqa: E402
 from time_lapack import ev_time  # noqa: E402
 
-for m in (512, 1024, 2048, 4096, 8192, 16384):
+for m in [int(x) for x in os.environ.get('SWEEP_M', '512,1024,2048,4096,8192,16384').split(',')]:
     P0 = PB.posit_from_f64(torch.from_numpy(SI.lu_matrix(m, 3)[:, :256].copy()).cuda())
     P = P0.clone()
     ipiv = torch.zeros(256, dtype=torch.int32, device="cuda")
