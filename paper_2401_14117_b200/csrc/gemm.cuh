@@ -40,7 +40,9 @@ namespace pg {
 // Ex + 30 and |Ep - Ec| as plain adds (ptxas emits IMAD.IADD / IADD3) instead
 // of IMADs with a register multiplier: C2 1149 -> 1173 Gflop/s on one box
 // (r03f/r03g A/B; moving the sign products or the zero-flag offset to the ALU
-// instead, or the table addresses to LEA, is slower)
+// instead, or the table addresses to LEA, is slower; so is the carry
+// normalisation c.M = Mn - cy 2^30 as an IMAD, r03y: extra three-register
+// IMADs cost more than the ALU slot they free)
 #ifndef PG_EXI_ALU
 #define PG_EXI_ALU 1
 #endif
