@@ -426,7 +426,9 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
 
 // ---- launchers (called from capi.cu) ----------------------------------------
 namespace {
-// Tile configurations (all 16 decoded accumulators per thread, 128 registers)
+// Tile configurations (all 16 decoded accumulators per thread, 128 registers).
+// 32 accumulators per thread in 256-thread CTAs lose (r03z: 64x128 as 4x8 per
+// thread 893, as 8x4 1118 vs 1171 Gflop/s on C2).
 using V1 = pg::Cfg<64, 64, 4, 4, 2, 96>;     // 256 thr, 2 CTAs / SM
 using V2 = pg::Cfg<64, 128, 4, 4, 1, 100>;   // 512 thr, 1 CTA / SM: the big trailing updates
 using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // 256 thr, 2 CTAs / SM: short-and-wide (LU TRSM updates)
