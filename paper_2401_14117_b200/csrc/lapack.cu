@@ -906,12 +906,25 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
     for (int jj = tid; jj < nrest; jj += NT) {            // thread per column j: its jb values are contiguous
       const int j = c0 + jb + jj;
       int f = 1;
-      for (int k = 0; k < jb; k++) {
-        const uint32_t x = L[(int64_t)j * ldl + c0 + k];
-        uint4 d;
-        const bool fk = fast_a(x, d);
-        S.ld[k][j] = make_uint4(d.x, d.y, d.z, x);
-        f &= (int)fk;
+      if (jb == W) {                                      // full block: all W loads in flight together
+        uint32_t xs[W];
+#pragma unroll
+        for (int k = 0; k < W; k++) xs[k] = L[(int64_t)j * ldl + c0 + k];
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+          uint4 d;
+          const bool fk = fast_a(xs[k], d);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, xs[k]);
+          f &= (int)fk;
+        }
+      } else {
+        for (int k = 0; k < jb; k++) {
+          const uint32_t x = L[(int64_t)j * ldl + c0 + k];
+          uint4 d;
+          const bool fk = fast_a(x, d);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, x);
+          f &= (int)fk;
+        }
       }
       S.colfast[j] = f;
     }
@@ -1053,7 +1066,18 @@ __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, i
       if ((int32_t)d <= 0) {                               // zero, negative or NaR pivot
         if (i == k) { fail = 1; *info = (int32_t)(row_base + k + 1); }
       } else if (in && i > k) {
-        lv_load(v, div(lv_pattern(v), d));
+        // decoded division by the shared divisor (one reciprocal), generic outside its range
+        pg::Acc dv;
+        const bool dok = pg::acc_decode(d, dv) && dv.E <= 37 && dv.E >= -37;
+        bool done = false;
+        if (dok && v.dec) {
+          done = pg::acc_div(v.a, dv.M, dv.E, dv.sg, __drcp_rn((double)dv.M) * 4294967296.0, pg::CalcConst());
+          if (done && !(v.a.E <= 75 && v.a.E >= -75) && v.a.E > pg::E_ZERO_LIMIT) {
+            v.pat = pg::acc_encode(v.a);
+            v.dec = false;
+          }
+        }
+        if (!done) lv_load(v, div(lv_pattern(v), d));
         const uint32_t x = lv_pattern(v);
         colp[i] = x;
         uint4 ad;
