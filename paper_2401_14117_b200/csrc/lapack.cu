@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(1024) k_iamax_key(int64_t m, const uint32_t* c
 // back: the global traffic is independent loads and stores.
 constexpr int SWP_MAX = 256;   // swaps per pass (longer ranges run in passes)
 constexpr int SWP_COLS = 32;
+constexpr int SWP_HASH_BITS = 10, SWP_HASH = 1 << SWP_HASH_BITS;   // >= 2 x SWP_MAX entries
 
 __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t ncols, int64_t k1, int64_t k2,
                                                const int32_t* ipiv, int64_t base) {
@@ -500,6 +501,8 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
   __shared__ int32_t tgt[SWP_MAX];      // pivot row of swap s (relative row index)
   __shared__ int16_t slot[SWP_MAX];     // slot holding that row
   __shared__ int16_t perm[2 * SWP_MAX]; // after the swaps, slot q holds the row gathered into slot perm[q]
+  __shared__ int hkey[SWP_HASH];        // pivot row -> first swap index using it (outside the block)
+  __shared__ int hval[SWP_HASH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * SWP_COLS + lane;
   for (int64_t s0 = k1; s0 < k2; s0 += SWP_MAX) {
@@ -507,17 +510,30 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
     for (int s = threadIdx.x; s < ns; s += blockDim.x) tgt[s] = ipiv[s0 + s] - 1 - (int32_t)base;
     __syncthreads();
     // slot of each pivot row: inside the block -> its own row slot; outside ->
-    // the slot of its first occurrence (ns + index), so repeated pivots share it
+    // the slot of its first occurrence (ns + index), so repeated pivots share it.
+    // First occurrences by a shared-memory hash (open addressing, atomicMin).
+    for (int h = threadIdx.x; h < SWP_HASH; h += blockDim.x) { hkey[h] = -1; hval[h] = 0x7FFFFFFF; }
+    __syncthreads();
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+      const int32_t p = tgt[s];
+      if (p >= s0 && p < s0 + ns) continue;
+      uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - SWP_HASH_BITS);
+      while (true) {
+        const int old = atomicCAS(&hkey[h], -1, p);
+        if (old == -1 || old == p) { atomicMin(&hval[h], s); break; }
+        h = (h + 1) & (SWP_HASH - 1);
+      }
+    }
+    __syncthreads();
     for (int s = threadIdx.x; s < ns; s += blockDim.x) {
       const int32_t p = tgt[s];
       int sl;
       if (p >= s0 && p < s0 + ns) {
         sl = (int)(p - s0);
       } else {
-        int f = s;
-        for (int t = 0; t < s; t++)
-          if (tgt[t] == p) { f = t; break; }
-        sl = ns + f;
+        uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - SWP_HASH_BITS);
+        while (hkey[h] != p) h = (h + 1) & (SWP_HASH - 1);
+        sl = ns + hval[h];
       }
       slot[s] = (int16_t)sl;
     }
@@ -540,17 +556,17 @@ __global__ void __launch_bounds__(256) k_laswp(uint32_t* A, int64_t lda, int64_t
       }
     } else {
       const int nwg = nw - 1, w = wid - 1;
-      for (int sb = w * 8; sb < ns; sb += nwg * 8) {
-        uint32_t v0[8], v1[8];
+      for (int sb = w * 16; sb < ns; sb += nwg * 16) {
+        uint32_t v0[16], v1[16];
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < 16; u++) {
           const int s = sb + u;
           const bool in = s < ns && c < ncols;
           v0[u] = in ? A[(s0 + s) * lda + c] : 0u;
           v1[u] = (in && slot[s] == ns + s) ? A[(int64_t)tgt[s] * lda + c] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < 16; u++) {
           const int s = sb + u;
           if (s < ns) {
             val[s][lane] = v0[u];
