@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
   extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long cbest;                // this CTA's best candidate key (next column)
+  __shared__ uint32_t srow[128];                      // the published rows p and j of the current column
   __shared__ uint4 urow[64];                          // the pivot row as decoded B operands {M, E, sg, fast}
   __shared__ uint32_t urowp[64];                      // ... and as patterns
   __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];      // the MAC's constant tables
@@ -393,22 +394,24 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
     grid.sync();
     const unsigned long long key = __ldcg(&ws->key[j]);
     const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
-    const uint32_t* rowp = ws->cand[par][p / rows_per_cta];
-    const uint32_t* rowj = ws->jrow[par];
-    const uint32_t v = __ldcg(rowp + j);
+    // rows p and j in one round trip (threads 0..W-1: row p; W..2W-1: row j)
+    if (tid < 2 * W)
+      srow[tid] = tid < W ? __ldcg(ws->cand[par][p / rows_per_cta] + tid) : __ldcg(ws->jrow[par] + (tid - W));
+    __syncthreads();
+    const uint32_t v = srow[j];
     if (blockIdx.x == 0 && tid == 0) {
       ipiv[j] = (int32_t)(row_base + p + 1);
       if (v == 0u && *info == 0) *info = (int32_t)(row_base + j + 1);
     }
     const bool swp = v != 0u && p != j;
     if (swp) {                                        // swap rows j and p (whole leaf width)
-      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = __ldcg(rowp + c);
-      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = __ldcg(rowj + c);
+      if (j >= rb && j < re) for (int c = tid; c < W; c += NT) tile[(j - rb) * W + c] = srow[c];
+      if (p >= rb && p < re) for (int c = tid; c < W; c += NT) tile[(p - rb) * W + c] = srow[W + c];
     }
-    const uint32_t* ursrc = swp ? rowp : rowj;        // the row now at position j
+    const int usrc = swp ? 0 : W;                     // the row now at position j
     for (int c = tid; c < W; c += NT) {
       LaneVal t;
-      const uint32_t x = __ldcg(ursrc + c);
+      const uint32_t x = srow[usrc + c];
       lv_load(t, x);
       urow[c] = make_uint4(t.a.M, (uint32_t)t.a.E, (uint32_t)t.a.sg, lv_operand(t) ? 1u : 0u);
       urowp[c] = x;
