@@ -1263,7 +1263,12 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     return e ? atoi(e) : 0;
   }();
   const bool wide = force ? force > 16 : allow_coop;
-  int nctas = wide ? nsm : (nsm < 16 ? nsm : 16);
+  static const int side_ctas = [] {              // side-stream leaf CTAs (1024 threads each)
+    const char* e = getenv("POSIT_SIDE_LEAF_CTAS");
+    const int v = e ? atoi(e) : 16;
+    return v > 0 ? v : 16;
+  }();
+  int nctas = wide ? nsm : (nsm < side_ctas ? nsm : side_ctas);
   int nthr = wide ? COOP_THREADS : 1024;
   if (force > 0 && force != 16 && force != 148) { nctas = force < nsm ? force : nsm; nthr = COOP_THREADS; }
   const int64_t rpc = (m + nctas - 1) / nctas;
