@@ -53,10 +53,14 @@ def test_from_to_f64_match_oracle(cuda_ok):
                                    1.0 + 2.0 ** -28, 2.0 ** 113, 3 * 2.0 ** 114])])
     got = to_host(PB.posit_from_f64(torch.from_numpy(xs).cuda()))
     assert mismatch(got, O.from_f64_array(xs)) == 0
+    got1 = to_host(PB.posit_from_f64(torch.from_numpy(xs).cuda()[1:]))    # 8-byte offset: the scalar path
+    assert mismatch(got1, O.from_f64_array(xs[1:])) == 0
     pats = np.concatenate([SI.edge_patterns(), SI.random_patterns(300000, 5)])
     back = PB.posit_to_f64(to_dev(pats)).cpu().numpy()
     ref = O.to_f64_array(pats)
     assert np.array_equal(back, ref, equal_nan=True)
+    back1 = PB.posit_to_f64(to_dev(pats)[1:]).cpu().numpy()
+    assert np.array_equal(back1, ref[1:], equal_nan=True)
 
 
 def test_exhaustive_roundtrip_2pow32_on_gpu(cuda_ok):
