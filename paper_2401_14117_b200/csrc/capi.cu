@@ -404,7 +404,8 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
         }
         if (s1 + b1 < n) {
           pg::Params Pr{m - s1, n - s1 - b1, b, L21, lda, U12 + b1, lda, A + s1 * lda + s1 + b1, lda, 1, 1, nullptr};
-          if ((rc = pb_launch_gemm(Pr, false, false, st))) return launch_check(rc);
+          // disjoint columns from the update just before it: may overlap its last wave
+          if ((rc = pb_launch_gemm(Pr, false, false, st, la))) return launch_check(rc);
         }
         if (!la &&
             (rc = pb_getrf_panel(m - s1, b1, A + s1 * lda + s1, lda, ipiv + s1, info, s1, work, true, st)))
@@ -474,7 +475,8 @@ int posit_potrf(char uplo, int64_t n, uint32_t* A, int64_t lda, int32_t* info, i
     if (s1 + b1 < n) {
       const uint32_t* L2b = A + (s1 + b1) * lda + s;
       pg::Params Pr{n - s1 - b1, n - s1 - b1, b, L2b, lda, L2b, lda, A + (s1 + b1) * lda + s1 + b1, lda, 1, 1, info};
-      if ((rc = pb_launch_gemm(Pr, true, true, st))) return launch_check(rc);
+      // disjoint columns from the block-column update just before it: may overlap its last wave
+      if ((rc = pb_launch_gemm(Pr, true, true, st, la))) return launch_check(rc);
     }
     if (!la && (rc = panel(st))) return launch_check(rc);
   }

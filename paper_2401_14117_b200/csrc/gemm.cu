@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   const int64_t gsize = (nbm - gfirst) < GROUP_M ? (nbm - gfirst) : GROUP_M;
   const int64_t row0 = (gfirst + (pid % per_group) % gsize) * BM;
   const int64_t col0 = ((pid % per_group) / gsize) * BN;
+  // let a programmatic-dependent successor (an independent update) start its
+  // CTAs on SMs this grid's last wave leaves idle
+  asm volatile("griddepcontrol.launch_dependents;");
   if (SYRK && col0 > row0 + BM - 1) return;   // tile entirely above the diagonal
   if (P.stop != nullptr && *P.stop != 0) return;
 
@@ -435,7 +438,7 @@ using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // 256 thr, 2 CTAs / SM: short-and-
 using V6 = pg::Cfg<128, 32, 4, 4, 2, 97>;    // 256 thr, 2 CTAs / SM: tall-and-narrow (Cholesky TRSM updates)
 
 template <class C>
-int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false) {
   const dim3 grid((unsigned)((P.n + C::BN - 1) / C::BN), (unsigned)((P.m + C::BM - 1) / C::BM));
   if (grid.y > 65535u) return PB_ERR_TOO_LARGE;
   const size_t smem = sizeof(typename C::Smem);
@@ -450,6 +453,23 @@ int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   }();
   (void)attrs;
   pb_count_launch();
+  if (pdl) {
+    // programmatic dependent launch: this grid may start while the previous
+    // kernel on the stream (which triggers at entry) runs its last wave; only
+    // for launches that do not read that kernel's output
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(C::NTHR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, P) == cudaSuccess) return 0;
+    (void)cudaGetLastError();
+  }
   kern<<<grid, C::NTHR, smem, st>>>(P);
   return 0;
 }
@@ -489,8 +509,13 @@ static int64_t tiny_outputs() {
   return v;
 }
 
-int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
+int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl) {
   if (P.m == 0 || P.n == 0) return 0;
+  static const int pdl_env = [] {
+    const char* e = getenv("POSIT_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  pdl = pdl && pdl_env != 0;
   // tiny shapes (the panel-internal updates): one thread per output
   static const int tiny_env = [] {
     const char* e = getenv("POSIT_GEMM_TINY");
@@ -514,10 +539,10 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st)
     if (w6 < best * 0.9) { v = 6; best = w6; }
   }
   switch (v) {
-    case 1: return launch_cfg<V1>(P, transb, syrk, st);
-    case 3: return launch_cfg<V3>(P, transb, syrk, st);
-    case 6: return launch_cfg<V6>(P, transb, syrk, st);
-    default: return launch_cfg<V2>(P, transb, syrk, st);
+    case 1: return launch_cfg<V1>(P, transb, syrk, st, pdl);
+    case 3: return launch_cfg<V3>(P, transb, syrk, st, pdl);
+    case 6: return launch_cfg<V6>(P, transb, syrk, st, pdl);
+    default: return launch_cfg<V2>(P, transb, syrk, st, pdl);
   }
 }
 

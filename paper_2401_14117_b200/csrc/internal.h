@@ -8,7 +8,9 @@
 
 namespace pg { struct Params; }
 
-int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
+// pdl: programmatic dependent launch after the previous kernel on st (only for
+// an update that does not read that kernel's output)
+int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false);
 int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
 int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);   // lapack.cu
 
