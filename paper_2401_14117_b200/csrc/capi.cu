@@ -325,6 +325,16 @@ static int lookahead_env() {
   return v;
 }
 
+static int64_t tail_w() {                       // POSIT_TAIL_W: width of the fused tail LU (0: off)
+  static const int64_t v = [] {
+    const char* e = getenv("POSIT_TAIL_W");
+    const int64_t w = e ? (int64_t)atoll(e) : (int64_t)512;   // r04l sweep: 512 best (C5 -1.7 ms, C4 -2.4 ms)
+    return w < 1024 ? w : (int64_t)1024;          // the fused kernel's widest leaf
+  }();
+  return v;
+}
+static int64_t tail_m() { return 148 * 40; }      // rows: 40 per CTA x 1024 columns fit 160 KB
+
 static int64_t wide_leaf_cols() {
   static const int64_t v = [] {
     const char* e = getenv("POSIT_WIDE_LEAF_COLS");
@@ -367,12 +377,27 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
   const bool la = lookahead_env() != 0 && kmax > nb;
   SideStream ss;
   if (la && (rc = ss.init())) return rc;
+  // the last <= tail_w() columns as one fused cooperative LU (then its swaps on the columns left of it)
+  auto fits_tail = [&](int64_t s0) { return tail_w() > 0 && n - s0 <= tail_w() && m - s0 <= tail_m(); };
+  auto run_tail = [&](int64_t s0) -> int {
+    int r = pb_getrf_tail(m - s0, n - s0, A + s0 * lda + s0, lda, ipiv + s0, info, s0, work, st);
+    if (r) return r;
+    if (s0 > 0 && (r = pb_laswp(s0, A, lda, s0, kmax, ipiv, 0, st))) return r;
+    return 0;
+  };
+  if (fits_tail(0)) {
+    if ((rc = run_tail(0)) == 0) return cuda_check(cudaPeekAtLastError());
+    if (rc != POSIT_ENOTSUP) return launch_check(rc);
+  }
   // panel 0 on the caller's stream
   if ((rc = pb_getrf_panel(m, kmax < nb ? kmax : nb, A, lda, ipiv, info, 0, work, true, st))) return launch_check(rc);
   for (int64_t s = 0; s < kmax; s += nb) {
     const int64_t b = (kmax - s) < nb ? (kmax - s) : nb;
     const int64_t s1 = s + b;                                  // next panel's first column / row
-    const int64_t b1 = (kmax - s1) < nb ? (kmax - s1) : nb;    // its width (<= 0: none)
+    int64_t b1 = (kmax - s1) < nb ? (kmax - s1) : nb;          // its width (<= 0: none)
+    // the rest after this step goes to the fused tail: update all of it now, no next panel
+    const bool tail_next = b1 > 0 && fits_tail(s1);
+    if (tail_next) b1 = 0;
     if (la && s > 0 && (rc = cuda_check(cudaStreamWaitEvent(st, ss.ev_panel, 0)))) return rc;
     // the panel's swaps on the columns left and right of it
     if (s > 0 && (rc = pb_laswp(s, A, lda, s, s1, ipiv, 0, st))) return launch_check(rc);
@@ -414,6 +439,10 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
         pg::Params P{m - s1, n - s1, b, L21, lda, U12, lda, A + s1 * lda + s1, lda, 1, 1, nullptr};
         if ((rc = pb_launch_gemm(P, false, false, st))) return launch_check(rc);
       }
+    }
+    if (tail_next) {
+      if ((rc = run_tail(s1))) return launch_check(rc);
+      break;
     }
   }
   return cuda_check(cudaPeekAtLastError());

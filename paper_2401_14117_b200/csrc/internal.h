@@ -18,6 +18,8 @@ int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_
 int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
                    int64_t row_base, void* ws, bool allow_coop, cudaStream_t st);
 size_t pb_panel_ws_bytes();
+int pb_getrf_tail(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
+                  void* ws, cudaStream_t st);
 int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
              int64_t ipiv_base, cudaStream_t st);
 int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st);

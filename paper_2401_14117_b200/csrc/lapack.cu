@@ -125,8 +125,9 @@ __device__ __forceinline__ void lv_fms_t(LaneVal& c, uint32_t ap, bool afast, co
 // ---- LU leaf (column by column, multi-CTA) ----------------------------------
 // Workspace: key[0..w) (uint64, zeroed per leaf) and a CTA counter.
 constexpr int LEAF_MAXCTA = 160;
+constexpr int TAIL_WMAX = 1024;   // widest leaf: the fused LU of a factorisation's last columns
 struct LeafWs {
-  unsigned long long key[64];
+  unsigned long long key[TAIL_WMAX];
   unsigned int done;
   uint32_t rowp[64];       // cooperative leaf: the pivot row and the current row, published
   uint32_t rowj[64];
@@ -134,6 +135,8 @@ struct LeafWs {
   // candidate row for the next column, and the row at the next diagonal position
   uint32_t cand[2][LEAF_MAXCTA][64];
   uint32_t jrow[2][64];
+  uint32_t tcand[2][LEAF_MAXCTA][TAIL_WMAX];   // the same for leaves up to TAIL_WMAX wide
+  uint32_t tjrow[2][TAIL_WMAX];
 };
 constexpr size_t LEAF_WS_ZERO = offsetof(LeafWs, cand);   // the part zeroed per leaf
 
@@ -338,26 +341,31 @@ __global__ void __launch_bounds__(1024) k_leaf_coop(uint32_t* A, int64_t lda, in
 // parity; after the sync the winner's candidate row IS the pivot row.  The
 // arithmetic per element is the decoded-domain update of k_leaf_coop, in the
 // same textbook order.
+// cand: [2][LEAF_MAXCTA][WMAX] candidate rows, jrow: [2][WMAX] diagonal rows
+template <int WMAX>
 __device__ __forceinline__ void leaf_publish(const uint32_t* tile, int W, int64_t rb, int nr, int64_t jn,
-                                             unsigned long long best, LeafWs* ws, int par, int tid, int NT) {
+                                             unsigned long long best, uint32_t* cand, uint32_t* jrow, int par,
+                                             int tid, int NT) {
   if (best != 0ull) {
     const int64_t r = (int64_t)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
     const int li = (int)(r - rb);
-    for (int c = tid; c < W; c += NT) ws->cand[par][blockIdx.x][c] = tile[li * W + c];
+    uint32_t* dst = cand + ((size_t)par * LEAF_MAXCTA + blockIdx.x) * WMAX;
+    for (int c = tid; c < W; c += NT) dst[c] = tile[li * W + c];
   }
   if (jn >= rb && jn < rb + nr)
-    for (int c = tid; c < W; c += NT) ws->jrow[par][c] = tile[(int)(jn - rb) * W + c];
+    for (int c = tid; c < W; c += NT) jrow[par * WMAX + c] = tile[(int)(jn - rb) * W + c];
 }
 
+template <int WMAX>
 __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, int64_t m, int64_t w,
                                                      int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
-                                                     int64_t row_base, LeafWs* ws) {
+                                                     int64_t row_base, LeafWs* ws, uint32_t* cand, uint32_t* jrow) {
   extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long cbest;                // this CTA's best candidate key (next column)
-  __shared__ uint32_t srow[128];                      // the published rows p and j of the current column
-  __shared__ uint4 urow[64];                          // the pivot row as decoded B operands {M, E, sg, fast}
-  __shared__ uint32_t urowp[64];                      // ... and as patterns
+  __shared__ uint32_t srow[2 * WMAX];                 // the published rows p and j of the current column
+  __shared__ uint4 urow[WMAX];                        // the pivot row as decoded B operands {M, E, sg, fast}
+  __shared__ uint32_t urowp[WMAX];                    // ... and as patterns
   __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];      // the MAC's constant tables
   const int NT = blockDim.x;
   cg::grid_group grid = cg::this_grid();
@@ -386,7 +394,7 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
       if (best != 0ull) atomicMax(&ws->key[0], best);
     }
     __syncthreads();
-    leaf_publish(tile, W, rb, nr, 0, cbest, ws, 0, tid, NT);
+    leaf_publish<WMAX>(tile, W, rb, nr, 0, cbest, cand, jrow, 0, tid, NT);
   }
   const int64_t jmax = m < w ? m : w;
   for (int64_t j = 0; j < jmax; j++) {
@@ -395,8 +403,11 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
     const unsigned long long key = __ldcg(&ws->key[j]);
     const int64_t p = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
     // rows p and j in one round trip (threads 0..W-1: row p; W..2W-1: row j)
-    if (tid < 2 * W)
-      srow[tid] = tid < W ? __ldcg(ws->cand[par][p / rows_per_cta] + tid) : __ldcg(ws->jrow[par] + (tid - W));
+    {
+      const uint32_t* cp = cand + ((size_t)par * LEAF_MAXCTA + (size_t)(p / rows_per_cta)) * WMAX;
+      const uint32_t* jp = jrow + par * WMAX;
+      for (int t = tid; t < 2 * W; t += NT) srow[t] = t < W ? __ldcg(cp + t) : __ldcg(jp + (t - W));
+    }
     __syncthreads();
     const uint32_t v = srow[j];
     if (blockIdx.x == 0 && tid == 0) {
@@ -460,7 +471,7 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
         if (best != 0ull) atomicMax(&ws->key[j + 1], best);
       }
       __syncthreads();
-      if (j + 1 < jmax) leaf_publish(tile, W, rb, nr, j + 1, cbest, ws, par ^ 1, tid, NT);
+      if (j + 1 < jmax) leaf_publish<WMAX>(tile, W, rb, nr, j + 1, cbest, cand, jrow, par ^ 1, tid, NT);
     }
     __syncthreads();
   }
@@ -1280,7 +1291,8 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
     if (!ok) c.coop = 0;
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(k_leaf_coop1, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_leaf_coop1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_leaf_coop1<TAIL_WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     return c;
   }();
   const int coop = cfg.coop, nsm = cfg.nsm;
@@ -1301,16 +1313,25 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
   if (force > 0 && force != 16 && force != 148) { nctas = force < nsm ? force : nsm; nthr = COOP_THREADS; }
   const int64_t rpc = (m + nctas - 1) / nctas;
   const size_t smem = (size_t)rpc * (size_t)w * sizeof(uint32_t);
-  if (coop && smem <= 160 * 1024 && w <= 64) {
+  if (coop && smem <= 160 * 1024 && w <= TAIL_WMAX) {
     int64_t mm = m, ww = w, rr = rpc, rbase = row_base, ld = lda;
-    void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws};
+    const bool wide_w = w > 64;
+    uint32_t* cand = wide_w ? &ws->tcand[0][0][0] : &ws->cand[0][0][0];
+    uint32_t* jrow = wide_w ? &ws->tjrow[0][0] : &ws->jrow[0][0];
+    void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws, &cand, &jrow};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
-    pb_count_launch();
-    // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known)
-    const void* kfn = (coop == 2 || grid > (unsigned)LEAF_MAXCTA) ? (const void*)k_leaf_coop : (const void*)k_leaf_coop1;
-    if (cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthr), args, smem, st) == cudaSuccess)
-      return last_launch();
-    (void)cudaGetLastError();                          // fall back to the per-column launches
+    // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known; w <= 64)
+    const void* kfn = nullptr;
+    if (grid <= (unsigned)LEAF_MAXCTA && (coop != 2 || wide_w))
+      kfn = wide_w ? (const void*)k_leaf_coop1<TAIL_WMAX> : (const void*)k_leaf_coop1<64>;
+    else if (!wide_w)
+      kfn = (const void*)k_leaf_coop;
+    if (kfn != nullptr) {
+      pb_count_launch();
+      if (cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthr), args, smem, st) == cudaSuccess)
+        return last_launch();
+      (void)cudaGetLastError();                        // fall back to the per-column launches
+    }
   }
   pb_count_launch();
   k_leaf_colmax<<<rows_grid(m, 256), 256, 0, st>>>(A, lda, m, ws);
@@ -1325,6 +1346,22 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     }
   }
   return last_launch();
+}
+
+// The fused tail: LU with partial pivoting of the whole remaining m x w block
+// (w <= TAIL_WMAX) as ONE cooperative right-looking launch (one grid sync per
+// column), instead of the last few blocked steps whose recursive panels are
+// latency-bound.  Same per-element order (Q6).  Returns POSIT_ENOTSUP when the
+// block does not fit the CTAs' shared memory (the caller keeps the blocked path).
+int pb_getrf_tail(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
+                  void* ws, cudaStream_t st) {
+  if (m <= 0 || w <= 0) return 0;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t rpc = (m + nsm - 1) / nsm;
+  if (w > TAIL_WMAX || (size_t)rpc * (size_t)w * sizeof(uint32_t) > 160 * 1024) return POSIT_ENOTSUP;
+  return getrf_leaf(m, w, A, lda, ipiv, info, row_base, static_cast<LeafWs*>(ws), true, st);
 }
 
 // Recursive panel LU (the traversal of LAPACK getrf2): factor the left half,

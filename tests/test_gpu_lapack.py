@@ -62,7 +62,10 @@ def test_getrf_config1_bit_exact(cuda_ok):
     assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv) and info == rinfo == 0
 
 
-@pytest.mark.parametrize("m,n,nb", [(100, 77, 16), (77, 100, 16), (300, 300, 64), (64, 64, 1), (130, 130, 256)])
+# n <= 512: the fused tail LU (one cooperative launch); n > 512: blocked steps
+# with lookahead, then the fused tail for the last <= 512 columns
+@pytest.mark.parametrize("m,n,nb", [(100, 77, 16), (77, 100, 16), (300, 300, 64), (64, 64, 1), (130, 130, 256),
+                                    (700, 650, 96), (650, 700, 64), (620, 620, 256), (1100, 1000, 256)])
 def test_getrf_ragged_and_block_sizes(cuda_ok, m, n, nb):
     A = _pats(np.random.default_rng(m + n).uniform(-1, 1, (m, n)))
     ref, rpiv, rinfo = O.getrf(A)
