@@ -112,7 +112,9 @@ int posit_gemm_naive(char transa, char transb, int64_t m, int64_t n, int64_t k, 
  * and m >= 1024 the work is pipelined in row chunks of C (internal streams and
  * events; B first, then each chunk's A and C rows up while the previous chunk
  * computes and the one before comes back); the result is bit-identical (row
- * chunks are independent outputs, Q6).  Returns after the copies complete. */
+ * chunks are independent outputs, Q6).  Returns after the copies complete.
+ * The pipeline's four streams and events are created on first use per host
+ * thread and device and kept for the process (no memory is held). */
 size_t posit_gemm_host_work_bytes(int64_t m, int64_t n, int64_t k);
 int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, uint32_t alpha,
                     const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta,

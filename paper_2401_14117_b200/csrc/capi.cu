@@ -142,36 +142,36 @@ static int gemm_host_pipelined(char transb, int64_t m, int64_t n, int64_t k, uin
   const int64_t rows = (((m + nch - 1) / nch) + 63) / 64 * 64;
   nch = (m + rows - 1) / rows;
   constexpr int MAXCH = 8;
-  cudaStream_t cs = nullptr, ds = nullptr, ks[2] = {nullptr, nullptr};
-  cudaEvent_t ev0 = nullptr, ev_in[MAXCH] = {}, ev_done[MAXCH] = {}, ev_end = nullptr;
-  int rc = 0;
-  auto cleanup = [&]() {
-    for (int i = 0; i < MAXCH; i++) {
-      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
-      if (ev_done[i]) cudaEventDestroy(ev_done[i]);
-    }
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev_end) cudaEventDestroy(ev_end);
-    if (cs) cudaStreamDestroy(cs);
-    if (ds) cudaStreamDestroy(ds);
-    for (auto& q : ks)
-      if (q) cudaStreamDestroy(q);
+  // streams and events are created once per host thread and device (creating
+  // them per call costs more than the copies they hide for small problems)
+  struct HostPipe {
+    cudaStream_t cs = nullptr, ds = nullptr, ks[2] = {nullptr, nullptr};
+    cudaEvent_t ev0 = nullptr, ev_end = nullptr, ev_in[MAXCH] = {}, ev_done[MAXCH] = {};
+    bool ok = false;
   };
+  thread_local HostPipe pipes[16];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return POSIT_ECUDA;
+  HostPipe& hp = pipes[dev];
+  int rc = 0;
   auto ck = [&](cudaError_t e) { if (e != cudaSuccess && rc == 0) rc = cuda_check(e); return rc == 0; };
-  if (!ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) || !ck(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking)) ||
-      !ck(cudaStreamCreateWithFlags(&ks[0], cudaStreamNonBlocking)) ||
-      !ck(cudaStreamCreateWithFlags(&ks[1], cudaStreamNonBlocking)) ||
-      !ck(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming)) ||
-      !ck(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming))) {
-    cleanup();
-    return rc;
+  if (!hp.ok) {
+    bool good = cudaStreamCreateWithFlags(&hp.cs, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&hp.ds, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&hp.ks[0], cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&hp.ks[1], cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&hp.ev0, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&hp.ev_end, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < MAXCH && good; i++)
+      good = cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&hp.ev_done[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!good) return cuda_check(cudaGetLastError());
+    hp.ok = true;
   }
-  for (int i = 0; i < nch; i++)
-    if (!ck(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming)) ||
-        !ck(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming))) {
-      cleanup();
-      return rc;
-    }
+  cudaStream_t cs = hp.cs, ds = hp.ds, ks[2] = {hp.ks[0], hp.ks[1]};
+  cudaEvent_t ev0 = hp.ev0, ev_end = hp.ev_end;
+  cudaEvent_t* ev_in = hp.ev_in;
+  cudaEvent_t* ev_done = hp.ev_done;
   // everything after the caller's earlier work on st
   ck(cudaEventRecord(ev0, st));
   for (cudaStream_t q : {cs, ds, ks[0], ks[1]}) ck(cudaStreamWaitEvent(q, ev0, 0));
@@ -201,7 +201,6 @@ static int gemm_host_pipelined(char transb, int64_t m, int64_t n, int64_t k, uin
   ck(cudaStreamWaitEvent(st, ev_end, 0));
   if (rc == 0) ck(cudaStreamSynchronize(st));
   else cudaStreamSynchronize(ds);
-  cleanup();
   return rc;
 }
 
