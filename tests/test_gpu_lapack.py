@@ -87,6 +87,24 @@ def test_getrf_special_cases(cuda_ok):
     assert rinfo == info == 21 and mismatch(got, ref) == 0 and np.array_equal(piv, rpiv)
 
 
+@pytest.mark.parametrize("zero_col", [100, 300, 650])
+def test_getrf_blocked_zero_pivot_and_specials(cuda_ok, zero_col):
+    # n > 512: blocked steps with lookahead (zero column inside a side-stream
+    # panel, or in the fused tail), NaR / zero / extreme entries elsewhere
+    n = 700
+    A = SI.lu_matrix(n, 21)
+    A[:, zero_col] = 0.0
+    A[5, 690] = np.nan                       # NaR: absorbing once column 690 is reached (after every zero_col)
+    A[400, 7] = 1e30
+    A[650, 320] = 1e-30
+    A[200, :] *= 2.0 ** 40
+    Ap = _pats(A)
+    ref, rpiv, rinfo = O.getrf(Ap)
+    got, piv, info = _gpu_getrf(Ap, 64)
+    assert rinfo == info == zero_col + 1
+    assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv)
+
+
 @pytest.mark.parametrize("s", [-16, -4, 0, 4, 16])
 def test_getrf_config5_scaling_small(cuda_ok, s):
     # configs[4] recipe (U[-1,1) seed 4 scaled by 2^s) at n = 384, nb = 64
