@@ -114,7 +114,7 @@ def test_getrf_config5_scaling_small(cuda_ok, s):
     assert mismatch(got, ref) == 0 and np.array_equal(piv, rpiv) and info == rinfo
 
 
-@pytest.mark.parametrize("n,nb", [(1, 1), (50, 16), (200, 64), (300, 256), (130, 32)])
+@pytest.mark.parametrize("n,nb", [(1, 1), (50, 16), (200, 64), (300, 256), (130, 32), (400, 64), (1100, 256)])
 def test_potrf_matches_oracle(cuda_ok, n, nb):
     A = _pats(SI.config3(n))
     ref, rinfo = O.potrf_lower(A)
@@ -135,6 +135,18 @@ def test_potrf_not_positive_definite(cuda_ok):
     assert info == rinfo == 46
     # the blocks before the failing block are fully defined and bit-identical
     assert mismatch(np.tril(got)[:, :32], np.tril(ref)[:, :32]) == 0
+
+
+def test_potrf_not_positive_definite_with_lookahead(cuda_ok):
+    # n >= 4 nb: side-stream panels; the failure is met inside a side-stream diagonal block
+    n, nb = 400, 64
+    A = SI.config3(n)
+    A[250, 250] = -1.0
+    Ap = _pats(A)
+    ref, rinfo = O.potrf_lower(Ap)
+    got, info = _gpu_potrf(Ap, nb)
+    assert info == rinfo == 251
+    assert mismatch(np.tril(got)[:, :192], np.tril(ref)[:, :192]) == 0
 
 
 @pytest.mark.parametrize("n", [1, 33, 300])
