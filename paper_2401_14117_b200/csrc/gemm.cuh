@@ -102,8 +102,25 @@ __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_
 // value = sg * M * 2^(E - 30), M hidden bit at 30; sg = +1 / -1 (int).
 struct Acc { uint32_t M; int32_t E; int32_t sg; };
 
+// The value is on the posit lattice (every producer rounds at f_s(E)), so for
+// |E| <= 107 the pattern is plain bit assembly in 32 bits: regime, the two
+// exponent bits (never truncated there), the top f_s = 29 - rl fraction bits
+// (the rest are zero).  Outside, the generic rounding encoder.
+#ifndef PG_FAST_ENCODE
+#define PG_FAST_ENCODE 1
+#endif
 __device__ __forceinline__ uint32_t acc_encode(const Acc& c) {
   if (c.M == 0u || c.E < -1000) return 0u;          // exact zero (see mac: scale far below range)
+#if PG_FAST_ENCODE
+  if (c.E <= 107 && c.E >= -107) {
+    const int32_t k = c.E >> 2;                     // floor(E / 4)
+    const uint32_t e = (uint32_t)c.E & 3u;
+    const int32_t rl = k >= 0 ? k + 2 : 1 - k;      // regime length incl. terminator, <= 28 here
+    const uint32_t reg = k >= 0 ? (0x7FFFFFFFu ^ (0x7FFFFFFFu >> (k + 1))) : (1u << (30 + k));
+    const uint32_t body = reg | (e << (29 - rl)) | ((c.M & 0x3FFFFFFFu) >> (rl + 1));
+    return c.sg < 0 ? 0u - body : body;
+  }
+#endif
   return p32::round_encode(c.sg < 0 ? 1u : 0u, c.E, (uint64_t)c.M << 33);
 }
 

@@ -211,3 +211,22 @@ def test_gemm_tiny_path_special_values(cuda_ok, transa, transb, alpha, beta):
         B = B.T.copy()
     ref = O.gemm(A, B, C, transa=transa, transb=transb, alpha=alpha, beta=beta)
     assert mismatch(_gpu_gemm(A, B, C, transb, alpha=alpha, beta=beta, transa=transa), ref) == 0
+
+
+def test_accumulator_encode_exhaustive_identity(cuda_ok):
+    # C <- C (-) 0 (x) B over all 2^32 patterns of C: every output goes through
+    # the accumulator decode and the exact lattice encoder (acc_encode) and must
+    # come back bit for bit (NaR stays NaR)
+    import torch
+    import paper_2401_14117_b200 as PB
+    side = 8192
+    A = torch.zeros(side, 1, dtype=torch.int32, device="cuda")
+    B = torch.full((1, side), 0x40000000, dtype=torch.int32, device="cuda")
+    bad = 0
+    for c0 in range(0, 1 << 32, side * side):
+        C0 = torch.arange(c0, c0 + side * side, dtype=torch.int64, device="cuda").to(torch.int32).view(side, side)
+        C = C0.clone()
+        PB.posit_gemm(A, B, C)
+        bad += int((C != C0).sum())
+        del C0, C
+    assert bad == 0
