@@ -12,9 +12,9 @@ namespace pg { struct Params; }
 // an update that does not read that kernel's output)
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false);
 int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
-int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);   // lapack.cu
+int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);   // chol.cu
 
-// lapack.cu
+// leaf.cu, swap.cu, trsm.cu, chol.cu, misc.cu
 int pb_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info,
                    int64_t row_base, void* ws, bool allow_coop, cudaStream_t st);
 size_t pb_panel_ws_bytes();

@@ -1,0 +1,559 @@
+// trsm.cu -- the two TRSM variants of the path: U12 =
+// L11^-1 A12 (left, lower, unit) and L21 = A21 L11^-T (right, lower,
+// transposed, non-unit).
+#include "lanes.cuh"
+
+namespace pl {
+
+// ---- TRSM in-block kernels (32-wide, right-looking across a warp) -----------
+// Unit lower, left: rows i0..i0+ib-1 of B (ib <= 32).  CTA = 32 warps = 32
+// columns; the 32 x 32 tile goes through shared memory (coalesced); warp w
+// owns column w with lane = row: step k broadcasts the final b_k by shuffle
+// and rows i > k apply b_i <- b_i (-) l_ik (x) b_k (ascending k per element).
+__global__ void __launch_bounds__(1024) k_trsm_llnu_blk(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t i0, int64_t ib, int64_t n) {
+  __shared__ uint32_t sb[TB][TB + 1];
+  __shared__ uint32_t sl[TB][TB + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * TB;
+  if (wid < ib) {
+    sl[wid][lane] = lane < wid ? L[(i0 + wid) * ldl + i0 + lane] : 0u;
+    sb[wid][lane] = (c0 + lane < n) ? B[(i0 + wid) * ldb + c0 + lane] : 0u;
+  }
+  __syncthreads();
+  LaneVal b;
+  lv_load(b, lane < ib ? sb[lane][wid] : 0u);
+  for (int k = 0; k < ib - 1; k++) {
+    const bool bf = lv_operand(b);
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, k);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, k);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, k);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, k) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, lane == k ? lv_pattern(b) : 0u, k);   // for the generic path
+    if (lane > k && lane < ib) {
+      const uint32_t ap = sl[lane][k];
+      uint4 ad;
+      const bool af = fast_a(ap, ad);
+      lv_fms(b, ap, af, ad, bM, bE, bs, bfk, bpk);
+    }
+  }
+  if (lane < ib) sb[lane][wid] = lv_pattern(b);
+  __syncthreads();
+  if (wid < ib && c0 + lane < n) B[(i0 + wid) * ldb + c0 + lane] = sb[wid][lane];
+}
+
+// The same, NW columns (warps) per CTA and L's block staged decoded: for
+// narrow right-hand sides (the panel-internal TRSMs) the 32-column CTA puts all
+// the (issue-bound) steps on one SM; 8-column CTAs spread them.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_trsm_llnu_blkw(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                           int64_t i0, int64_t ib, int64_t n) {
+  __shared__ uint32_t sb[TB][NW + 1];
+  __shared__ uint4 sld[TB][TB];           // L[i0 + r][i0 + c] decoded A-format {M, E, sigma (0: slow), pattern}
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * NW;
+  for (int r = wid; r < ib; r += NW) {
+    const uint32_t x = lane < r ? L[(i0 + r) * ldl + i0 + lane] : 0u;
+    uint4 d;
+    const bool f = fast_a(x, d);
+    sld[r][lane] = make_uint4(d.x, d.y, f ? d.z : 0u, x);
+    if (lane < NW) sb[r][lane] = (c0 + lane < n) ? B[(i0 + r) * ldb + c0 + lane] : 0u;
+  }
+  __syncthreads();
+  LaneVal b;
+  lv_load(b, lane < ib ? sb[lane][wid] : 0u);
+  for (int k = 0; k < ib - 1; k++) {
+    const bool bf = lv_operand(b);
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, k);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, k);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, k);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, k) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, lane == k ? lv_pattern(b) : 0u, k);   // for the generic path
+    if (lane > k && lane < ib) {
+      const uint4 ad = sld[lane][k];
+      lv_fms(b, ad.w, ad.z != 0u, ad, bM, bE, bs, bfk, bpk);
+    }
+  }
+  if (lane < ib) sb[lane][wid] = lv_pattern(b);
+  __syncthreads();
+  for (int r = wid; r < ib; r += NW)
+    if (lane < NW && c0 + lane < n) B[(i0 + r) * ldb + c0 + lane] = sb[r][lane];
+}
+
+// The same in-block solve with one thread per column of B (default).  Columns
+// are independent, so a thread runs its column's substitution alone: rows in
+// groups of LC_G, each group first taking the updates from every earlier
+// (final) row of the block in ascending k -- LC_G independent MAC chains -- and
+// then the in-group triangle, still ascending k per element (Q6).  No shuffles
+// and no idle lanes.  The MACs run branch-free in k-slabs of <= 16 (the
+// GEMM's exactness argument, csrc/gemm.cuh: operands |E| <= 37, accumulators
+// |E| <= 75 at the slab start); a slab whose operands or accumulators fall
+// outside runs the generic pattern path instead.  L's 32 x 32 block is staged
+// decoded (read as a broadcast); a column's final rows stay in the thread's
+// own shared slots.
+constexpr int LC_T = 32, LC_SLAB = 16;
+
+__device__ __forceinline__ void lc_renorm(LaneVal& v) {
+  if (v.dec && !(v.a.E <= 75 && v.a.E >= -75) && v.a.E > pg::E_ZERO_LIMIT) {
+    v.pat = pg::acc_encode(v.a);
+    v.dec = false;
+  }
+}
+
+template <int LC_G>
+__global__ void __launch_bounds__(LC_T) k_trsm_llnu_col(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t i0, int64_t ib, int64_t n, int one) {
+  __shared__ uint4 sl[TB][TB];          // L[i0 + r][i0 + c] decoded A-format {M, E, sigma, pattern}
+  __shared__ uint4 sb[TB][LC_T];        // final rows of each thread's column: B-format {M, E, sg, pattern}
+  __shared__ uint32_t ps[LC_G][LC_T];   // generic path: the group's values as patterns
+  __shared__ uint32_t lmask[TB];        // bit c of row r: L[r][c] is a fast operand (rows >= ib: all ones)
+  __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];
+  const int lane = threadIdx.x;
+  const int64_t col = (int64_t)blockIdx.x * LC_T + lane;
+  const bool live = col < n;
+  pg::fill_tables(tp, tx, lane, LC_T);
+  // stage L's block (row r: lane = column, coalesced) and the column's ib
+  // values of B: all loads first (in flight together), then decode L in place
+  // with the fast masks by ballot (a compact loop: this code runs once)
+#pragma unroll
+  for (int r = 0; r < TB; r++) {
+    sl[r][lane].w = r >= ib ? 0x40000000u : (lane < r ? L[(i0 + r) * ldl + i0 + lane] : 0u);   // rows >= ib: dummy 1.0
+    sb[r][lane].w = (live && r < ib) ? B[(i0 + r) * ldb + col] : 0u;     // the input, until row r is final
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int r = 0; r < TB; r++) {
+    const uint32_t x = sl[r][lane].w;
+    uint4 d;
+    const bool f = fast_a(x, d);
+    sl[r][lane] = make_uint4(d.x, d.y, d.z, x);
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+    if (lane == 0) lmask[r] = r >= ib ? 0xFFFFFFFFu : (bal & ((1u << r) - 1u));
+  }
+  pg::MacConst K;
+  K.one = (uint32_t)one;
+  K.sixteen = 16u * K.one;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(tx + pg::TBIAS) - 30u * 16u;
+  __syncthreads();
+  if (!live) return;
+  uint32_t bmask = 0u;                    // bit k: final row k is a fast B operand
+  for (int g0 = 0; g0 < ib; g0 += LC_G) {
+    LaneVal v[LC_G];
+    uint32_t lg = 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < LC_G; u++) {
+      lv_load(v[u], sb[g0 + u][lane].w);
+      lg &= lmask[g0 + u];
+    }
+    // the updates from the final rows k < g0, ascending k, in slabs
+    for (int k0 = 0; k0 < g0; k0 += LC_SLAB) {
+      const int kn = (g0 - k0) < LC_SLAB ? (g0 - k0) : LC_SLAB;
+      const uint32_t sm = ((1u << kn) - 1u) << k0;
+      bool ok = (bmask & sm) == sm && (lg & sm) == sm;
+#pragma unroll
+      for (int u = 0; u < LC_G; u++) ok = ok && v[u].dec;
+      if (ok) {
+        for (int k = k0; k < k0 + kn; k++) {
+          const uint4 bk = sb[k][lane];
+          uint32_t bad = 0u;
+#pragma unroll
+          for (int u = 0; u < LC_G; u++) {
+            const uint4 ad = sl[g0 + u][k];
+            pg::mac<pg::MacConst, false>(v[u].a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bk.x, (int32_t)bk.y,
+                                         -(int32_t)bk.z, K, bad);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) lc_renorm(v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) ps[u][lane] = lv_pattern(v[u]);
+#pragma unroll 1
+        for (int k = k0; k < k0 + kn; k++) {
+          const uint32_t bp = sb[k][lane].w;
+#pragma unroll 1
+          for (int u = 0; u < LC_G; u++) ps[u][lane] = sub(ps[u][lane], mul(sl[g0 + u][k].w, bp));
+        }
+#pragma unroll
+        for (int u = 0; u < LC_G; u++) lv_load(v[u], ps[u][lane]);
+      }
+    }
+    // the in-group triangle: row g0 + u is final once its predecessors are
+    int ugen = LC_G;
+#pragma unroll
+    for (int u = 0; u < LC_G; u++) {
+      if (ugen == LC_G) {
+        const bool opf = lv_operand(v[u]);
+        bool ok = opf;
+#pragma unroll
+        for (int w = u + 1; w < LC_G; w++) ok = ok && v[w].dec && ((lmask[g0 + w] >> (g0 + u)) & 1u);
+        if (!ok) {
+          ugen = u;
+        } else {
+          const uint32_t pat = pg::acc_encode(v[u].a);
+          sb[g0 + u][lane] = make_uint4(v[u].a.M, (uint32_t)v[u].a.E, (uint32_t)v[u].a.sg, pat);
+          bmask |= 1u << (g0 + u);
+          if (g0 + u < ib) B[(i0 + g0 + u) * ldb + col] = pat;
+          uint32_t bad = 0u;
+#pragma unroll
+          for (int w = u + 1; w < LC_G; w++) {
+            const uint4 ad = sl[g0 + w][g0 + u];
+            pg::mac<pg::MacConst, false>(v[w].a, ad.x, (int32_t)ad.y, (int32_t)ad.z, v[u].a.M, v[u].a.E, -v[u].a.sg,
+                                         K, bad);
+          }
+        }
+      }
+    }
+    if (ugen < LC_G) {                    // the rest of the triangle on patterns
+#pragma unroll
+      for (int u = 0; u < LC_G; u++)
+        if (u >= ugen) ps[u][lane] = lv_pattern(v[u]);
+#pragma unroll 1
+      for (int u = ugen; u < LC_G; u++) {
+        const uint32_t pat = ps[u][lane];
+        LaneVal f;
+        lv_load(f, pat);
+        const bool opf = lv_operand(f);
+        sb[g0 + u][lane] = make_uint4(f.a.M, (uint32_t)f.a.E, (uint32_t)f.a.sg, pat);
+        if (opf) bmask |= 1u << (g0 + u);
+        if (g0 + u < ib) B[(i0 + g0 + u) * ldb + col] = pat;
+#pragma unroll 1
+        for (int w = u + 1; w < LC_G; w++) ps[w][lane] = sub(ps[w][lane], mul(sl[g0 + w][g0 + u].w, pat));
+      }
+    }
+  }
+}
+
+// Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 16).
+// Half-warp per row of B (two rows per warp), lane = column (coalesced):
+// step k finalises b_k <- b_k (/) l_kk, broadcasts it within the half-warp,
+// and columns j > k apply b_j <- b_j (-) b_k (x) l_jk (ascending k).
+constexpr int TBR = 16;
+
+__global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                        int64_t j0, int64_t jb, int64_t m, const int32_t* stop) {
+  __shared__ uint32_t sl[TBR][TBR + 1];
+  if (stop != nullptr && *stop != 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int col = lane & (TBR - 1), half = lane & TBR;
+  if (threadIdx.x < TBR * TBR) {
+    const int rr = threadIdx.x / TBR, cc = threadIdx.x % TBR;
+    if (rr < jb) sl[rr][cc] = cc <= rr ? L[(j0 + rr) * ldl + j0 + cc] : 0u;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * 64 + wid * 2 + (half ? 1 : 0);
+  if ((int64_t)blockIdx.x * 64 + wid * 2 >= m) return;          // whole warp out of range
+  const bool live = r < m && col < jb;
+  LaneVal b;
+  lv_load(b, live ? B[r * ldb + j0 + col] : 0u);
+  for (int k = 0; k < jb; k++) {
+    if (col == k && live) lv_load(b, div(lv_pattern(b), sl[k][k]));
+    const bool bf = lv_operand(b);
+    const int src = half | k;
+    const uint32_t bM = __shfl_sync(0xFFFFFFFFu, b.a.M, src);
+    const int32_t bE = __shfl_sync(0xFFFFFFFFu, b.a.E, src);
+    const int32_t bs = __shfl_sync(0xFFFFFFFFu, b.a.sg, src);
+    const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, src) != 0;
+    const uint32_t bpk = __shfl_sync(0xFFFFFFFFu, col == k ? lv_pattern(b) : 0u, src);   // for the generic path
+    if (live && col > k) {
+      const uint32_t ap = sl[col][k];
+      uint4 ad;
+      const bool af = fast_a(ap, ad);
+      lv_fms(b, ap, af, ad, bM, bE, bs, bfk, bpk);
+    }
+  }
+  if (live) B[r * ldb + j0 + col] = lv_pattern(b);
+}
+
+// ---- fused right TRSM (Cholesky L21 = A21 L11^-T), n <= 256 ----------------
+// Rows of B are independent, so one CTA solves FR_ROWS whole rows: B's tile
+// lives in shared memory (patterns); per W-column block J a group of W lanes
+// per row runs the in-block substitution (lane = column, as k_trsm_rltn_blk),
+// publishes the block's W final values decoded, and every thread then updates
+// its own columns of the later blocks with them (the fast MAC with the
+// GEMM's shared-memory constant tables; L's block column staged decoded,
+// k-major so a lane group reads consecutive words).  Per element the updates
+// still arrive one at a time in ascending k (Q6).
+constexpr int FR_NMAX = 256, FR_W = 16;
+
+template <int W, int FR_ROWS>
+struct FrSmem {
+  uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
+  uint4 ld[W][FR_NMAX];                       // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
+  uint4 bop[FR_ROWS][W];                      // block J's final values, B-format {M, E, sg (0: slow), pattern}
+  uint32_t lblk[W][W + 1];                    // L's diagonal block J (patterns)
+  uint4 lblkd[W][W];                          // the same, decoded A-format {M, E, sigma, fast}
+  uint4 ldiag[W];                             // L[c0 + k][c0 + k] as a divisor {M hidden@30, E, sg, fast}
+  double ldrcp[W];                            // RN(2^32 / M) of each diagonal divisor
+  int colfast[FR_NMAX];                       // column j's staged L values all fast-path operands
+  int rowfast[FR_ROWS];                       // row r's block-J values all fast-path operands
+  uint4 tp[pg::TSIZE];                        // the MAC's per-scale constant tables
+  uint4 tx[pg::TSIZE];
+};
+
+template <int W, int FR_ROWS>
+__global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
+                                                                 int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
+                                                                 int one) {
+  constexpr int NT = FR_ROWS * W;
+  extern __shared__ __align__(16) unsigned char fr_raw[];
+  FrSmem<W, FR_ROWS>& S = *reinterpret_cast<FrSmem<W, FR_ROWS>*>(fr_raw);
+  if (stop != nullptr && *stop != 0) return;
+  const int tid = threadIdx.x;
+  const int r = tid / W, c = tid % W;                  // row of the tile, column within a block
+  const int grp = (tid & 31) & ~(W - 1);               // first lane of this row's lane group
+  const int64_t r0 = (int64_t)blockIdx.x * FR_ROWS;
+  const int64_t rows = (m - r0) < FR_ROWS ? (m - r0) : FR_ROWS;
+  pg::fill_tables(S.tp, S.tx, tid, NT);
+  pg::MacConst K;
+  K.one = (uint32_t)one; K.sixteen = 16u * K.one;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
+  for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
+    const int rr = e / (int)n, cc = e % (int)n;
+    S.b[rr][cc] = rr < rows ? B[(r0 + rr) * ldb + cc] : 0u;
+  }
+  const int nblk = (int)((n + W - 1) / W);
+  for (int J = 0; J < nblk; J++) {
+    const int c0 = J * W;
+    const int jb = (int)((n - c0) < W ? (n - c0) : W);
+    __syncthreads();
+    // stage: L's diagonal block J (patterns) and L[j][c0 + k] for j >= c0 + jb (decoded)
+    for (int e = tid; e < W * W; e += NT) {
+      const int rr = e / W, cc = e % W;
+      if (rr < jb && cc <= rr) {
+        const uint32_t x = L[(c0 + rr) * ldl + c0 + cc];
+        S.lblk[rr][cc] = x;
+        uint4 d;
+        const bool f = fast_a(x, d);
+        S.lblkd[rr][cc] = make_uint4(d.x, d.y, d.z, f ? 1u : 0u);
+        if (rr == cc) {
+          pg::Acc a;
+          const bool ok = pg::acc_decode(x, a) && x != 0u && a.E <= 37 && a.E >= -37;
+          S.ldiag[rr] = make_uint4(a.M, (uint32_t)a.E, (uint32_t)a.sg, ok ? 1u : 0u);
+          S.ldrcp[rr] = ok ? __drcp_rn((double)a.M) * 4294967296.0 : 0.0;
+        }
+      }
+    }
+    const int nrest = (int)n - c0 - jb;
+    for (int jj = tid; jj < nrest; jj += NT) {            // thread per column j: its jb values are contiguous
+      const int j = c0 + jb + jj;
+      int f = 1;
+      if (jb == W) {                                      // full block: all W loads in flight together
+        uint32_t xs[W];
+#pragma unroll
+        for (int k = 0; k < W; k++) xs[k] = L[(int64_t)j * ldl + c0 + k];
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+          uint4 d;
+          const bool fk = fast_a(xs[k], d);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, xs[k]);
+          f &= (int)fk;
+        }
+      } else {
+        for (int k = 0; k < jb; k++) {
+          const uint32_t x = L[(int64_t)j * ldl + c0 + k];
+          uint4 d;
+          const bool fk = fast_a(x, d);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, x);
+          f &= (int)fk;
+        }
+      }
+      S.colfast[j] = f;
+    }
+    __syncthreads();
+    // in-block substitution: W lanes per row, lane = column
+    {
+      const bool live = r < rows && c < jb;
+      LaneVal v;
+      lv_load(v, live ? S.b[r][c0 + c] : 0u);
+      for (int k = 0; k < jb; k++) {
+        if (c == k && live) {
+          const uint4 dv = S.ldiag[k];
+          bool done = false;
+          if (v.dec && dv.w != 0u) done = pg::acc_div(v.a, dv.x, (int32_t)dv.y, (int32_t)dv.z, S.ldrcp[k], K);
+          if (done) {
+            if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
+          } else {
+            lv_load(v, div(lv_pattern(v), S.lblk[k][k]));
+          }
+        }
+        const bool bf = lv_operand(v);
+        const int src = grp | k;
+        const uint32_t bM = __shfl_sync(0xFFFFFFFFu, v.a.M, src);
+        const int32_t bE = __shfl_sync(0xFFFFFFFFu, v.a.E, src);
+        const int32_t bs = __shfl_sync(0xFFFFFFFFu, v.a.sg, src);
+        const bool bfk = __shfl_sync(0xFFFFFFFFu, (int)bf, src) != 0;
+        const bool bdk = __shfl_sync(0xFFFFFFFFu, (int)v.dec, src) != 0;
+        const uint32_t bpraw = __shfl_sync(0xFFFFFFFFu, v.pat, src);
+        if (live && c > k) {
+          const uint4 ad = S.lblkd[c][k];
+          if (ad.w != 0u && bfk && v.dec) {
+            uint32_t bad = 0u;
+            pg::mac(v.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bs, K, bad);
+            if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
+          } else {
+            pg::Acc bk{bM, bE, bs};
+            const uint32_t bp = bdk ? pg::acc_encode(bk) : bpraw;        // b_k's pattern (rare path)
+            lv_load(v, sub(lv_pattern(v), mul(S.lblk[c][k], bp)));
+          }
+        }
+      }
+      const bool opf = lv_operand(v) || !live;
+      const unsigned grpmask = (W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u)) << grp;
+      const bool allf = (__ballot_sync(0xFFFFFFFFu, opf) & grpmask) == grpmask;
+      if (live) {
+        const uint32_t x = lv_pattern(v);
+        S.b[r][c0 + c] = x;
+        S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), x);   // sign pre-negated: c (-) a b
+      }
+      if (c == 0) S.rowfast[r] = allf ? 1 : 0;
+    }
+    __syncthreads();
+    // updates of the later blocks: thread (r, c) owns columns c0 + jb + c + W t.
+    // A column whose k-loop has only fast operands and an accumulator within
+    // |E| <= 75 stays inside the MAC's exact range for all jb <= 16 steps
+    // (|Ep| <= 75, |E| grows by <= 1 per step, cancellation stops at >= -106).
+    // Four of the thread's columns are advanced together (independent chains
+    // for ILP); a group with any slow column runs the generic path.
+    if (r < rows) {
+      const bool rf = S.rowfast[r] != 0;
+      constexpr int G = 4;
+      for (int col0 = c0 + jb + c; col0 < (int)n; col0 += G * W) {
+        pg::Acc a[G];
+        uint32_t x[G];
+        bool ok = rf;
+#pragma unroll
+        for (int u = 0; u < G; u++) {
+          const int col = col0 + u * W;
+          const bool in = col < (int)n;
+          x[u] = in ? S.b[r][col] : 0u;
+          const bool d = pg::acc_decode(x[u], a[u]) && (x[u] == 0u || (a[u].E <= 75 && a[u].E >= -75));
+          ok = ok && d && (!in || S.colfast[col] != 0);
+        }
+        if (ok) {
+          uint32_t bad = 0u;
+#pragma unroll 2
+          for (int k = 0; k < jb; k++) {
+            const uint4 bd = S.bop[r][k];
+#pragma unroll
+            for (int u = 0; u < G; u++) {
+              const uint4 ad = S.ld[k][min(col0 + u * W, (int)n - 1)];
+              pg::mac(a[u], ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x, (int32_t)bd.y, (int32_t)bd.z, K, bad);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < G; u++)
+            if (col0 + u * W < (int)n) S.b[r][col0 + u * W] = pg::acc_encode(a[u]);
+        } else {
+#pragma unroll 1
+          for (int u = 0; u < G; u++) {
+            const int col = col0 + u * W;
+            if (col >= (int)n) break;
+            uint32_t y = x[u];
+            for (int k = 0; k < jb; k++) y = sub(y, mul(S.ld[k][col].w, S.bop[r][k].w));
+            S.b[r][col] = y;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
+    const int rr = e / (int)n, cc = e % (int)n;
+    if (rr < rows) B[(r0 + rr) * ldb + cc] = S.b[rr][cc];
+  }
+}
+
+}  // namespace pl
+
+using namespace pl;
+
+int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  // thread per column (row groups of 4; -1 = auto) once the columns fill the
+  // SMs: one such launch costs ~46 us whatever its width up to 592 warps,
+  // the warp-per-column kernel ~34 us per wave of 148 CTAs (r02v launch lists)
+  static const int col_env = [] {
+    const char* e = getenv("POSIT_LLNU_COL");
+    const int v = e == nullptr ? -1 : atoi(e);
+    return v == 0 || v == 4 || v == 8 ? v : -1;
+  }();
+  const int use_col = col_env >= 0 ? col_env : (n > 148 * TB ? 4 : 0);
+  static const int blk_env = [] {                 // warp-per-column CTA width: 8 (default) or 32 columns
+    const char* e = getenv("POSIT_LLNU_BLK");
+    return e ? atoi(e) : 8;
+  }();
+  for (int64_t i0 = 0; i0 < m; i0 += TB) {
+    const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
+    if (ib > 1) {
+      pb_count_launch();
+      if (use_col == 8)
+        k_trsm_llnu_col<8><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
+      else if (use_col == 4)
+        k_trsm_llnu_col<4><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
+      else if (blk_env == 8)
+        k_trsm_llnu_blkw<8><<<(unsigned)((n + 7) / 8), 256, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+      else
+        k_trsm_llnu_blk<<<(unsigned)((n + TB - 1) / TB), 1024, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+    }
+    if (i0 + ib < m) {
+      pg::Params P{m - i0 - ib, n, ib, L + (i0 + ib) * ldl + i0, ldl, B + i0 * ldb, ldb, B + (i0 + ib) * ldb, ldb,
+                   1, 1, nullptr};
+      const int rc = pb_launch_gemm(P, false, false, st);
+      if (rc) return rc;
+    }
+  }
+  return last_launch();
+}
+
+int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb, const int32_t* stop,
+                 cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  if (n <= FR_NMAX) {
+    // one fused launch: each CTA solves FR_ROWS whole rows
+    // variant: W lanes per row x FR_ROWS rows per CTA (env POSIT_RLTN = "W,ROWS")
+    static const int var = [] {
+      const char* e = getenv("POSIT_RLTN");
+      int w = 16, r = 16;
+      if (e) sscanf(e, "%d,%d", &w, &r);
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 16>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 32>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<8, 16>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<8, 32>));
+      return w * 100 + r;
+    }();
+    pb_count_launch();
+#define PB_RLTN(W_, R_)                                                                                              \
+  k_trsm_rltn_fused<W_, R_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(L, ldl, B, ldb, m, \
+                                                                                                   n, stop, 1)
+    if (var == 1632) PB_RLTN(16, 32);
+    else if (var == 816) PB_RLTN(8, 16);
+    else if (var == 832) PB_RLTN(8, 32);
+    else PB_RLTN(16, 16);
+#undef PB_RLTN
+    return last_launch();
+  }
+  for (int64_t j0 = 0; j0 < n; j0 += TBR) {
+    const int64_t jb = (n - j0) < TBR ? (n - j0) : TBR;
+    pb_count_launch();
+    k_trsm_rltn_blk<<<(unsigned)((m + 63) / 64), 1024, 0, st>>>(L, ldl, B, ldb, j0, jb, m, stop);
+    if (j0 + jb < n) {
+      // B[:, j0+jb:] -= B[:, j0:j0+jb] * L[j0+jb:, j0:j0+jb]^T   (NT GEMM, K = jb)
+      pg::Params P{m, n - j0 - jb, jb, B + j0, ldb, L + (j0 + jb) * ldl + j0, ldl, B + j0 + jb, ldb, 1, 1, stop};
+      const int rc = pb_launch_gemm(P, true, false, st);
+      if (rc) return rc;
+    }
+  }
+  return last_launch();
+}
+
+// Recursive diagonal-block Cholesky (the traversal of LAPACK potrf2): leaf
+// blocks of <= 32 in shared memory, TRSM + SYRK between them.  Every stage
+// is a no-op once *info != 0.
+
