@@ -13,6 +13,10 @@
 namespace pg {
 
 constexpr int KK_UNROLL = PG_KK_UNROLL;   // k-steps of the fast loop unrolled (each TM x TN MACs)
+#ifndef PG_KK_UNROLL_SYRK
+#define PG_KK_UNROLL_SYRK 1   // r04z / r05a: SYRK 1135 -> 1141 Gflop/s, C3 184.5 -> 183.6 ms
+#endif
+constexpr int KK_UNROLL_SYRK = PG_KK_UNROLL_SYRK;   // the same for the SYRK instantiations
 #ifndef PG_CPASYNC
 #define PG_CPASYNC 1
 #endif
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           acc[i][j].E = min(acc[i][j].E, E_CLAMP);
         }
       if (kmax == BK) {
-#pragma unroll (KK_UNROLL)
+#pragma unroll (SYRK ? KK_UNROLL_SYRK : KK_UNROLL)
         for (int kk = 0; kk < BK; kk++) {
           uint4 av[TM], bv[TN];
 #pragma unroll
