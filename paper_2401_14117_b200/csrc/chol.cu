@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(256) k_syrk_tiny(int64_t n, int64_t k, const u
   C[i * ldc + j] = lv_pattern(c);
 }
 
+// Diagonal-block Cholesky: right-looking by 32-wide block columns (leaf of
+// <= 32 in one CTA, the rows below by the fused TRSM, the trailing lower
+// triangle by the one-thread-per-element SYRK), or (POSIT_POTF2=0) the
+// recursive potrf2 traversal.  Every stage is a no-op once *info != 0.
 int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_base, cudaStream_t st) {
   if (b <= 0) return 0;
   static const int mode = [] {                   // 1: blocked right-looking, 32-wide (default); 0: recursive

@@ -552,8 +552,3 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   }
   return last_launch();
 }
-
-// Recursive diagonal-block Cholesky (the traversal of LAPACK potrf2): leaf
-// blocks of <= 32 in shared memory, TRSM + SYRK between them.  Every stage
-// is a no-op once *info != 0.
-
