@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <initializer_list>
+#include <utility>
 #include "gemm.cuh"
 #include "internal.h"
 
@@ -433,13 +435,20 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
 
 // ---- launchers (called from capi.cu) ----------------------------------------
 namespace {
-// Tile configurations (all 16 decoded accumulators per thread, 128 registers).
-// 32 accumulators per thread in 256-thread CTAs lose (r03z: 64x128 as 4x8 per
-// thread 893, as 8x4 1118 vs 1171 Gflop/s on C2).
-using V1 = pg::Cfg<64, 64, 4, 4, 2, 96>;     // 256 thr, 2 CTAs / SM
-using V2 = pg::Cfg<64, 128, 4, 4, 1, 100>;   // 512 thr, 1 CTA / SM: the big trailing updates
-using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // 256 thr, 2 CTAs / SM: short-and-wide (LU TRSM updates)
-using V6 = pg::Cfg<128, 32, 4, 4, 2, 97>;    // 256 thr, 2 CTAs / SM: tall-and-narrow (Cholesky TRSM updates)
+// Tile configurations.  The GEMM (non-SYRK) tiles use 4 x 2 accumulators per
+// thread, so 32 warps are resident per SM (64 registers each): more warps hide
+// the pipe contention of the MAC's integer stream better than a 4 x 4 tile's
+// extra ILP (r05g-r05i: C2 1171 -> 1194 Gflop/s; 2 x 4 per thread 1020, 4 x 8
+// per thread 893).  The SYRK tiles keep 4 x 4 per thread (the 64 x 64 one is
+// the best SYRK: 1165 vs 1152 for 4 x 2).
+using V1 = pg::Cfg<64, 64, 4, 4, 2, 96>;     // SYRK: 256 thr, 2 CTAs / SM (the SYRK default)
+using V2 = pg::Cfg<64, 128, 4, 4, 1, 100>;   // SYRK: 512 thr, 1 CTA / SM
+using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // SYRK: 256 thr, 2 CTAs / SM, short-and-wide
+using V6 = pg::Cfg<128, 32, 4, 4, 2, 97>;    // SYRK: 256 thr, 2 CTAs / SM, tall-and-narrow
+using G1 = pg::Cfg<64, 128, 4, 2, 1, 100>;   // GEMM: 1024 thr, 1 CTA / SM (the GEMM default)
+using G2 = pg::Cfg<64, 64, 4, 2, 2, 99>;     // GEMM: 512 thr, 2 CTAs / SM
+using G3 = pg::Cfg<32, 128, 4, 2, 2, 99>;    // GEMM: 512 thr, 2 CTAs / SM, short-and-wide (LU TRSM updates)
+using G4 = pg::Cfg<128, 32, 4, 2, 2, 99>;    // GEMM: 512 thr, 2 CTAs / SM, tall-and-narrow (Cholesky TRSM updates)
 
 template <class C>
 int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false) {
@@ -498,7 +507,7 @@ double model_time(int64_t m, int64_t n, bool syrk) {
   const int64_t per_sm = (tiles + 147) / 148;
   const int64_t resident = (per_sm < C::MINB ? per_sm : C::MINB) * C::NTHR;
   const double rate = (resident >= 512 ? 1.0 : 0.66) * C::EFF;
-  return (double)per_sm * C::NTHR * 16.0 / rate;
+  return (double)per_sm * C::BM * C::BN / rate;
 }
 }  // namespace
 
@@ -534,19 +543,32 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st,
   if (tiny_env == 2 && P.k >= 1 && P.k <= 32 && P.n <= 32 && !syrk) return pb_launch_gemm_tiny(P, transb, syrk, st);
   int v = variant();
   if (v == 0) {
-    const double w2 = model_time<V2>(P.m, P.n, syrk), w1 = model_time<V1>(P.m, P.n, syrk);
-    const double w3 = model_time<V3>(P.m, P.n, syrk), w6 = model_time<V6>(P.m, P.n, syrk);
-    v = 2;
-    double best = w2;
-    if (w1 < best * 0.9) { v = 1; best = w1; }
-    if (w3 < best * 0.9) { v = 3; best = w3; }
-    if (w6 < best * 0.9) { v = 6; best = w6; }
+    // the smallest modelled time; near-ties (within 10%) go to the first candidate
+    auto pick = [&](int v0, double w0, std::initializer_list<std::pair<int, double>> rest) {
+      int vb = v0;
+      double best = w0;
+      for (const auto& c : rest)
+        if (c.second < best * 0.9) { vb = c.first; best = c.second; }
+      return vb;
+    };
+    if (syrk)
+      v = pick(1, model_time<V1>(P.m, P.n, true),
+               {{2, model_time<V2>(P.m, P.n, true)}, {3, model_time<V3>(P.m, P.n, true)},
+                {6, model_time<V6>(P.m, P.n, true)}});
+    else
+      v = pick(11, model_time<G1>(P.m, P.n, false),
+               {{12, model_time<G2>(P.m, P.n, false)}, {13, model_time<G3>(P.m, P.n, false)},
+                {14, model_time<G4>(P.m, P.n, false)}});
   }
   switch (v) {
     case 1: return launch_cfg<V1>(P, transb, syrk, st, pdl);
+    case 2: return launch_cfg<V2>(P, transb, syrk, st, pdl);
     case 3: return launch_cfg<V3>(P, transb, syrk, st, pdl);
     case 6: return launch_cfg<V6>(P, transb, syrk, st, pdl);
-    default: return launch_cfg<V2>(P, transb, syrk, st, pdl);
+    case 12: return launch_cfg<G2>(P, transb, syrk, st, pdl);
+    case 13: return launch_cfg<G3>(P, transb, syrk, st, pdl);
+    case 14: return launch_cfg<G4>(P, transb, syrk, st, pdl);
+    default: return launch_cfg<G1>(P, transb, syrk, st, pdl);
   }
 }
 
