@@ -9,7 +9,7 @@
 #include "internal.h"
 
 #ifndef PG_KK_UNROLL
-#define PG_KK_UNROLL 2
+#define PG_KK_UNROLL 4   // with the 4 x 2 tiles (r05l: C2 1194 -> 1197; unroll 2 was best for 4 x 4)
 #endif
 
 namespace pg {
