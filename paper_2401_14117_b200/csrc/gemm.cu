@@ -122,6 +122,8 @@ template <class C, bool TRANS_B, bool SYRK>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, TM = C::TM, TN = C::TN, NTHR = C::NTHR;
   constexpr int AQ = C::AQ, BQ = C::BQ;
+  // product table by Ea + Eb for the 16-warp (4 x 4) tiles, by Ep for the 32-warp (4 x 2) ones (r05p)
+  constexpr bool PBS = (PG_PROD_BY_SUM != 0) && (TM * TN >= 16);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(smem_raw);
 
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   if (P.stop != nullptr && *P.stop != 0) return;
 
   const uint32_t flip = P.neg ? 1u : 0u;
-  fill_tables(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
+  fill_tables<PBS>(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
   MacConst K;
   K.one = (uint32_t)P.one; K.sixteen = 16u * K.one;
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + TBIAS);
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       } else {
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       }

@@ -146,23 +146,30 @@ constexpr uint32_t BAD_FLAG = 1u << 23;  // accumulated with IMAD; checked once 
 constexpr int E_CLAMP = 150;             // accumulator scales are clamped per k-slab (table bounds)
 constexpr int E_ZERO_LIMIT = -1000;      // scales below this encode an exact zero accumulator
 
+// PBS: the product table indexed by Ea + Eb (both normalisation variants in one
+// entry, so the lookup overlaps the multiply) or by the normalised scale Ep
+// (one instruction fewer per MAC, the lookup after the multiply).  The first
+// suits the 16-warp tiles, the second the 32-warp ones (r05p), so each kernel
+// fills the table its MAC reads.
+template <bool PBS = (PG_PROD_BY_SUM != 0)>
 __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int nthr) {
   for (int i = tid; i < TSIZE; i += nthr) {
     const int E = i - TBIAS;
     uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     const bool fast = t <= (uint32_t)T_FAST_MAX;
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;        // keep the product constants finite
-#if PG_PROD_BY_SUM
-    // indexed by S = Ea + Eb: {2^(30 - t0), 2^(29 - t1) - 2^(30 - t0), 2^(t0 + 3), 2^(t1 + 3) - 2^(t0 + 3)}
-    // with t0 = t(S) (product normalised at n = 0) and t1 = t(S + 1) (n = 1)
-    const int E1 = E + 1;
-    uint32_t t1 = (uint32_t)(E1 ^ (E1 >> 31)) >> 2;
-    t1 = t1 < (uint32_t)T_FAST_MAX ? t1 : (uint32_t)T_FAST_MAX;
-    tp[i] = make_uint4(1u << (30 - tc), (1u << (29 - t1)) - (1u << (30 - tc)), 1u << (tc + 3),
-                       (1u << (t1 + 3)) - (1u << (tc + 3)));
-#else
-    tp[i] = make_uint4(1u << (30 - tc), 0u - (1u << (29 - tc)), 1u << (tc + 3), 0u);
-#endif
+    if constexpr (PBS) {
+      // indexed by S = Ea + Eb: {2^(30 - t0), 2^(29 - t1) - 2^(30 - t0), 2^(t0 + 3), 2^(t1 + 3) - 2^(t0 + 3)}
+      // with t0 = t(S) (product normalised at n = 0) and t1 = t(S + 1) (n = 1)
+      const int E1 = E + 1;
+      uint32_t t1 = (uint32_t)(E1 ^ (E1 >> 31)) >> 2;
+      t1 = t1 < (uint32_t)T_FAST_MAX ? t1 : (uint32_t)T_FAST_MAX;
+      tp[i] = make_uint4(1u << (30 - tc), (1u << (29 - t1)) - (1u << (30 - tc)), 1u << (tc + 3),
+                         (1u << (t1 + 3)) - (1u << (tc + 3)));
+    } else {
+      // indexed by Ep: {2^(30 - t), -2^(29 - t), 2^(t + 3), 0}
+      tp[i] = make_uint4(1u << (30 - tc), 0u - (1u << (29 - tc)), 1u << (tc + 3), 0u);
+    }
     tx[i] = make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
   }
 }
@@ -255,23 +262,26 @@ struct CalcConst {
 // The GEMM does not track per MAC: with |Ea|, |Eb| <= 37 (staging) and
 // |Ec| <= 91 at the slab start, |Ep| <= 75, a sum's scale grows by at most 1
 // per MAC (<= 107 after 16) and cancellation stops at Ebg - 31 >= -106.
-template <class Tab, bool TRACK = true, bool PRE = false>
+template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0)>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
   uint32_t hi, lo;
   mulwide(Ma, Mb, hi, lo);                            // hi in [2^29, 2^31)
   const uint32_t n = hi >> 30;
-#if PG_PROD_BY_SUM
-  // the table lookup depends only on Ea + Eb, so it overlaps the multiply
-  const uint4 T = PRE ? lds128(aw + bw) : K.prod2(Ea + Eb);
-  const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
-  const uint32_t mulp = fmad(n, T.w, T.z);
-#else
-  const int32_t Ep = Ea + Eb + (int32_t)n;            // IADD3 (ALU / FMA balance)
-  const uint4 T = K.prod(Ep);
-  const uint32_t mulp = T.z;
-#endif
+  uint4 T;
+  int32_t Ep;
+  uint32_t mulp;
+  if constexpr (PBS) {
+    // the table lookup depends only on Ea + Eb, so it overlaps the multiply
+    T = PRE ? lds128(aw + bw) : K.prod2(Ea + Eb);
+    Ep = Ea + Eb + (int32_t)n;                        // IADD3 (ALU / FMA balance)
+    mulp = fmad(n, T.w, T.z);
+  } else {
+    Ep = Ea + Eb + (int32_t)n;
+    T = K.prod(Ep);
+    mulp = T.z;
+  }
   // drop D = t + 2 + n bits of hi: hi * 2^(32 - D) splits into q (high) and the dropped bits (low, left-aligned)
   uint32_t qp, yp;
   mulwide(hi, fmad(n, T.y, T.x), qp, yp);
