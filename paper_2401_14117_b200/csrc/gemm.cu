@@ -437,20 +437,15 @@ __global__ void k_gemm_naive(Params P, int transb, int syrk) {
 
 // ---- launchers (called from capi.cu) ----------------------------------------
 namespace {
-// Tile configurations.  The GEMM (non-SYRK) tiles use 4 x 2 accumulators per
-// thread, so 32 warps are resident per SM (64 registers each): more warps hide
-// the pipe contention of the MAC's integer stream better than a 4 x 4 tile's
-// extra ILP (r05g-r05i: C2 1171 -> 1194 Gflop/s; 2 x 4 per thread 1020, 4 x 8
-// per thread 893).  The SYRK tiles keep 4 x 4 per thread (the 64 x 64 one is
-// the best SYRK: 1165 vs 1152 for 4 x 2).
-using V1 = pg::Cfg<64, 64, 4, 4, 2, 96>;     // SYRK: 256 thr, 2 CTAs / SM (the SYRK default)
-using V2 = pg::Cfg<64, 128, 4, 4, 1, 100>;   // SYRK: 512 thr, 1 CTA / SM
-using V3 = pg::Cfg<32, 128, 4, 4, 2, 98>;    // SYRK: 256 thr, 2 CTAs / SM, short-and-wide
-using V6 = pg::Cfg<128, 32, 4, 4, 2, 97>;    // SYRK: 256 thr, 2 CTAs / SM, tall-and-narrow
-using G1 = pg::Cfg<64, 128, 4, 2, 1, 100>;   // GEMM: 1024 thr, 1 CTA / SM (the GEMM default)
-using G2 = pg::Cfg<64, 64, 4, 2, 2, 99>;     // GEMM: 512 thr, 2 CTAs / SM
-using G3 = pg::Cfg<32, 128, 4, 2, 2, 99>;    // GEMM: 512 thr, 2 CTAs / SM, short-and-wide (LU TRSM updates)
-using G4 = pg::Cfg<128, 32, 4, 2, 2, 99>;    // GEMM: 512 thr, 2 CTAs / SM, tall-and-narrow (Cholesky TRSM updates)
+// Tile configurations: 4 x 2 accumulators per thread (64 registers), so 32
+// warps are resident per SM -- more warps hide the pipe contention of the
+// MAC's integer stream better than a 4 x 4 tile's extra ILP (r05g-r05i, r05q:
+// C2 1171 -> 1200 Gflop/s, SYRK 1165 -> 1179; 2 x 4 per thread ~1020, 4 x 8
+// per thread 893).
+using G1 = pg::Cfg<64, 128, 4, 2, 1, 100>;   // 1024 thr, 1 CTA / SM (the GEMM default)
+using G2 = pg::Cfg<64, 64, 4, 2, 2, 99>;     // 512 thr, 2 CTAs / SM (the SYRK default)
+using G3 = pg::Cfg<32, 128, 4, 2, 2, 99>;    // 512 thr, 2 CTAs / SM, short-and-wide (LU TRSM updates)
+using G4 = pg::Cfg<128, 32, 4, 2, 2, 99>;    // 512 thr, 2 CTAs / SM, tall-and-narrow (Cholesky TRSM updates)
 
 template <class C>
 int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false) {
@@ -553,20 +548,12 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st,
         if (c.second < best * 0.9) { vb = c.first; best = c.second; }
       return vb;
     };
-    if (syrk)
-      v = pick(1, model_time<V1>(P.m, P.n, true),
-               {{2, model_time<V2>(P.m, P.n, true)}, {3, model_time<V3>(P.m, P.n, true)},
-                {6, model_time<V6>(P.m, P.n, true)}});
-    else
-      v = pick(11, model_time<G1>(P.m, P.n, false),
-               {{12, model_time<G2>(P.m, P.n, false)}, {13, model_time<G3>(P.m, P.n, false)},
-                {14, model_time<G4>(P.m, P.n, false)}});
+    const int base = syrk ? 12 : 11;
+    v = pick(base, base == 12 ? model_time<G2>(P.m, P.n, syrk) : model_time<G1>(P.m, P.n, syrk),
+             {{base == 12 ? 11 : 12, base == 12 ? model_time<G1>(P.m, P.n, syrk) : model_time<G2>(P.m, P.n, syrk)},
+              {13, model_time<G3>(P.m, P.n, syrk)}, {14, model_time<G4>(P.m, P.n, syrk)}});
   }
   switch (v) {
-    case 1: return launch_cfg<V1>(P, transb, syrk, st, pdl);
-    case 2: return launch_cfg<V2>(P, transb, syrk, st, pdl);
-    case 3: return launch_cfg<V3>(P, transb, syrk, st, pdl);
-    case 6: return launch_cfg<V6>(P, transb, syrk, st, pdl);
     case 12: return launch_cfg<G2>(P, transb, syrk, st, pdl);
     case 13: return launch_cfg<G3>(P, transb, syrk, st, pdl);
     case 14: return launch_cfg<G4>(P, transb, syrk, st, pdl);
