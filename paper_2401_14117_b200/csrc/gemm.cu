@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   constexpr int AQ = C::AQ, BQ = C::BQ;
   // product table by Ea + Eb for the 16-warp (4 x 4) tiles, by Ep for the 32-warp (4 x 2) ones (r05p)
   constexpr bool PBS = (PG_PROD_BY_SUM != 0) && (TM * TN >= 16);
+  constexpr bool CEM = PG_CECM == 2 || (PG_CECM == 1 && C::MINB == 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(smem_raw);
 
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   const uint32_t flip = P.neg ? 1u : 0u;
   fill_tables<PBS>(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
   MacConst K;
-  K.one = (uint32_t)P.one; K.sixteen = 16u * K.one;
+  K.one = (uint32_t)P.one; K.sixteen = 16u * K.one; K.m2p30 = 0xC0000000u * K.one;
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + TBIAS);
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + TBIAS) - 30u * 16u;   // indexed by Ex + 30
 
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       } else {
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       }

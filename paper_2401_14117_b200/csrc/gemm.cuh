@@ -58,6 +58,9 @@ namespace pg {
 #ifndef PG_PRESCALED             // product table address = Aw + Bw (staged 16 E [+ base]) instead of an IMAD:
 #define PG_PRESCALED 0           // one instruction fewer per MAC but an ALU add (C2 1167 vs 1173, r03i) -> off
 #endif
+#ifndef PG_CECM                  // CEM tail of the MAC (see mac) in the one-CTA-per-SM GEMM tiles: 1 on, 0 off,
+#define PG_CECM 1                // 2 in every tile (r05u: C2 1199 -> 1205, the 2-CTA SYRK tile 1178 -> 1151)
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -206,6 +209,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 // Table access for the GEMM: the two shared-memory tables.
 struct MacConst {
   uint32_t one, sixteen;               // = 1, 16 at run time (opaque to ptxas)
+  uint32_t m2p30 = 0xC0000000u;        // -2^30 (the CEM tail; set from `one` by the kernel)
   uint32_t tp0, tx0;                   // shared-memory byte addresses of table entry E = 0 (tx: Ex + 30 = 0)
 #if PG_TAB_ADDR_PLAIN == 2
   // IMAD with an immediate multiplier (two register reads instead of three)
@@ -232,6 +236,7 @@ struct MacConst {
 // the panel-side kernels, where latency rather than issue rate matters.
 struct CalcConst {
   uint32_t one = 1u;
+  uint32_t m2p30 = 0xC0000000u;
   __device__ __forceinline__ uint4 prod(int32_t Ep) const {
     uint32_t t = (uint32_t)(Ep ^ (Ep >> 31)) >> 2;
     t = t < (uint32_t)T_FAST_MAX ? t : (uint32_t)T_FAST_MAX;
@@ -262,7 +267,10 @@ struct CalcConst {
 // The GEMM does not track per MAC: with |Ea|, |Eb| <= 37 (staging) and
 // |Ec| <= 91 at the slab start, |Ep| <= 75, a sum's scale grows by at most 1
 // per MAC (<= 107 after 16) and cancellation stops at Ebg - 31 >= -106.
-template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0)>
+// CEM: the sum's carry renormalisation as an IMAD (Mn - cy 2^30) and the
+// cancellation offset as flo & 0xFFFFF000 inside the scale add: 1.2
+// instructions per MAC fewer, one FMA-pipe op fewer, ALU count unchanged.
+template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0), bool CEM = false>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
@@ -342,14 +350,20 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
       : "=r"(rx) : "r"(yx | (qx & 1u)), "r"(qx), "r"(U.x));
   const uint32_t Mn = fmad(rx, U.y, 0u);                      // hidden@30, or 2^31 on carry
   const uint32_t cy = Mn >> 31;
-  c.M = Mn >> cy;
+  if constexpr (CEM) c.M = fmad(cy, K.m2p30, Mn);            // 2^31 -> 2^30 (IMAD instead of a shift)
+  else c.M = Mn >> cy;
   // exact cancellation (x == 0, flo = -1): scale pushed far below any product,
   // so the (zero) accumulator is the small operand of every later add
+  if constexpr (CEM) {
+    // flo in [0, 31] -> 0, flo = 0xFFFFFFFF -> 0xFFFFF000 = -4096: one LOP3 + one IADD3
+    c.E = (int32_t)(U.w + cy + (flo & 0xFFFFF000u));
+  } else {
 #if PG_CE_ALU
   c.E = (int32_t)(U.w + cy) + (((int32_t)flo >> 31) & -4096);
 #else
   c.E = (int32_t)fmad((uint32_t)((int32_t)flo >> 31), 4096u, U.w + cy);
 #endif
+  }
   c.sg = sbg;
   if (TRACK) badacc = fmad(U.z, K.one, badacc);               // BAD_FLAG bits accumulate
 }

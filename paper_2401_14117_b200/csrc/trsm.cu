@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64
 // GEMM's shared-memory constant tables; L's block column staged decoded,
 // k-major so a lane group reads consecutive words).  Per element the updates
 // still arrive one at a time in ascending k (Q6).
-constexpr int FR_NMAX = 256, FR_W = 16;
+constexpr int FR_NMAX = 256;
 
 template <int W, int FR_ROWS>
 struct FrSmem {

@@ -6,11 +6,12 @@ Counts the instructions of every backward-branch loop that contains IMAD.HI
 before spending GPU time.
 """
 import collections
+import os
 import re
 import subprocess
 import sys
 
-LIB = "/root/repo/paper_2401_14117_b200/libposit_b200.so"
+LIB = os.environ.get("POSIT_LIB_PATH", "/root/repo/paper_2401_14117_b200/libposit_b200.so")
 
 
 def main():
