@@ -45,7 +45,7 @@ struct Cfg {
     uint32_t ra[BM * BK];                 // raw patterns of the next slab (cp.async target, by quad)
     uint32_t rb[BK * BN];
 #endif
-    uint4 tp[TSIZE];
+    uint4 tp[2 * TSIZE];                  // PIX: 2 entries per scale; else the first TSIZE
     uint4 tx[TSIZE];
   };
 };
@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   constexpr int AQ = C::AQ, BQ = C::BQ;
   // product table by Ea + Eb for the 16-warp (4 x 4) tiles, by Ep for the 32-warp (4 x 2) ones (r05p)
   constexpr bool PBS = (PG_PROD_BY_SUM != 0) && (TM * TN >= 16);
-  constexpr bool CEM = PG_CECM == 2 || (PG_CECM == 1 && C::MINB == 1);
+  constexpr bool CEM = PG_CECM == 2 || (PG_CECM == 1 && C::MINB == 1) || (PG_CECM == 3 && C::MINB > 1);
+  constexpr bool PIX = !PBS && (PG_PIX == 2 || (PG_PIX == 1 && C::MINB == 1));
+  constexpr uint32_t WM = PIX ? 32u : 16u;   // staged .w = WM E (+ table base on the B side)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(smem_raw);
 
@@ -147,10 +149,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   if (P.stop != nullptr && *P.stop != 0) return;
 
   const uint32_t flip = P.neg ? 1u : 0u;
-  fill_tables<PBS>(S.tp, S.tx, tid, NTHR);           // visible after the first __syncthreads_or
+  fill_tables<PBS, !PIX>(S.tp, S.tx, tid, NTHR);     // visible after the first __syncthreads_or
+  if constexpr (PIX) fill_prod_pix(S.tp, tid, NTHR);
   MacConst K;
   K.one = (uint32_t)P.one; K.sixteen = 16u * K.one; K.m2p30 = 0xC0000000u * K.one;
-  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + TBIAS);
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + (PIX ? 2 * TBIAS : TBIAS));
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + TBIAS) - 30u * 16u;   // indexed by Ex + 30
 
   // ---- accumulators -------------------------------------------------------
@@ -210,11 +213,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (!P.transa) {
         const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+        for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31, WM>(ra[h * 4 + q], 0u, sp);
       } else {
         const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.a[buf][ak][ar + q] = stage_decode<31>(ra[h * 4 + q], 0u, sp);
+        for (int q = 0; q < 4; q++) S.a[buf][ak][ar + q] = stage_decode<31, WM>(ra[h * 4 + q], 0u, sp);
       }
     }
 #pragma unroll
@@ -224,11 +227,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (!TRANS_B) {
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30>(rb[h * 4 + q], flip, sp, K.tp0);
+        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30, WM>(rb[h * 4 + q], flip, sp, K.tp0);
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30>(rb[h * 4 + q], flip, sp, K.tp0);
+        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30, WM>(rb[h * 4 + q], flip, sp, K.tp0);
       }
     }
     return sp;
@@ -283,14 +286,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         const int64_t av = P.k - (k0 + ak);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.a[buf][ak + q][ar] = stage_decode<31>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+          S.a[buf][ak + q][ar] = stage_decode<31, WM>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
       } else {
         const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
         const bool rok = k0 + ak < P.k;
         const int64_t av = P.m - (row0 + ar);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.a[buf][ak][ar + q] = stage_decode<31>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+          S.a[buf][ak][ar + q] = stage_decode<31, WM>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
       }
     }
 #pragma unroll
@@ -303,14 +306,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         const int64_t av = P.n - (col0 + bc);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk][bc + q] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
+          S.b[buf][bk][bc + q] = stage_decode<30, WM>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
         const bool rok = col0 + bc < P.n;
         const int64_t av = P.k - (k0 + bk);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk + q][bc] = stage_decode<30>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
+          S.b[buf][bk + q][bc] = stage_decode<30, WM>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
       }
     }
     return sp;
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       } else {
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
                                                       (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
         }
       }

@@ -58,8 +58,11 @@ namespace pg {
 #ifndef PG_PRESCALED             // product table address = Aw + Bw (staged 16 E [+ base]) instead of an IMAD:
 #define PG_PRESCALED 0           // one instruction fewer per MAC but an ALU add (C2 1167 vs 1173, r03i) -> off
 #endif
-#ifndef PG_CECM                  // CEM tail of the MAC (see mac) in the one-CTA-per-SM GEMM tiles: 1 on, 0 off,
-#define PG_CECM 1                // 2 in every tile (r05u: C2 1199 -> 1205, the 2-CTA SYRK tile 1178 -> 1151)
+#ifndef PG_CECM                  // CEM tail of the MAC (see mac): 0 off, 1 in the one-CTA-per-SM tile, 2 in every
+#define PG_CECM 3                // tile, 3 in the two-CTA tiles (r05x, with PIX: 1-CTA 1242 off / 1237 on, 2-CTA
+#endif                           // SYRK 1204 off / 1210 on; before PIX it was the other way round, r05u)
+#ifndef PG_PIX                   // PIX product table (see fill_prod_pix): 1 one-CTA-per-SM tile, 2 every tile, 0 off
+#define PG_PIX 2
 #endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
@@ -85,7 +88,7 @@ struct Params {
 // A side: significand hidden bit at 31.  B side: hidden bit at 30.
 // Staged element = {M, E, sigma (+1 / -1 as int), 0}.  Returns "special"
 // (zero, NaR, |E| > 53) through `special`.
-template <int HID>
+template <int HID, uint32_t WM = 16u>
 __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_t& special, uint32_t wbase = 0u) {
   const uint32_t s = (x >> 31) ^ flip;
   const uint32_t a = (x >> 31) ? (0u - x) : x;
@@ -98,7 +101,7 @@ __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_
   const uint32_t M = (0x80000000u | ((rest << 2) >> 1)) >> (31 - HID);
   special |= (uint32_t)((x << 1) == 0u) | (uint32_t)(E > E_STAGE_MAX) | (uint32_t)(E < -E_STAGE_MAX);
   // .w: 16 E + wbase, so that a product's table address is one add of the two operands' .w (PG_PRESCALED)
-  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, (uint32_t)E * 16u + wbase);
+  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, (uint32_t)E * WM + wbase);
 }
 
 // ---- accumulator <-> pattern (exact: the accumulator is on the lattice) ----
@@ -154,14 +157,15 @@ constexpr int E_ZERO_LIMIT = -1000;      // scales below this encode an exact ze
 // (one instruction fewer per MAC, the lookup after the multiply).  The first
 // suits the 16-warp tiles, the second the 32-warp ones (r05p), so each kernel
 // fills the table its MAC reads.
-template <bool PBS = (PG_PROD_BY_SUM != 0)>
+template <bool PBS = (PG_PROD_BY_SUM != 0), bool TP = true>
 __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int nthr) {
   for (int i = tid; i < TSIZE; i += nthr) {
     const int E = i - TBIAS;
     uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     const bool fast = t <= (uint32_t)T_FAST_MAX;
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;        // keep the product constants finite
-    if constexpr (PBS) {
+    if constexpr (!TP) {
+    } else if constexpr (PBS) {
       // indexed by S = Ea + Eb: {2^(30 - t0), 2^(29 - t1) - 2^(30 - t0), 2^(t0 + 3), 2^(t1 + 3) - 2^(t0 + 3)}
       // with t0 = t(S) (product normalised at n = 0) and t1 = t(S + 1) (n = 1)
       const int E1 = E + 1;
@@ -174,6 +178,22 @@ __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int n
       tp[i] = make_uint4(1u << (30 - tc), 0u - (1u << (29 - tc)), 1u << (tc + 3), 0u);
     }
     tx[i] = make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
+  }
+}
+
+// PIX product table (the GEMM's one-CTA-per-SM tile): indexed by S = Ea + Eb
+// and the product's normalisation bit n, interleaved (entry 2 (S + TBIAS) + n),
+// so the address is one IMAD of n over the staged operands' prescaled sum
+// (.w = 32 E [+ base]), and the entry carries the multiplier that splits off
+// the dropped bits (n folded in), the renormalising power and Ep = S + n:
+//   { 2^(30 - n - t), 0, 2^(t + 3), S + n },  t = t(S + n)
+__device__ __forceinline__ void fill_prod_pix(uint4* tp, int tid, int nthr) {
+  for (int i = tid; i < 2 * TSIZE; i += nthr) {
+    const uint32_t n = (uint32_t)i & 1u;
+    const int E = (i >> 1) - TBIAS + (int)n;
+    uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
+    t = t < (uint32_t)T_FAST_MAX ? t : (uint32_t)T_FAST_MAX;
+    tp[i] = make_uint4(1u << (30 - n - t), 0u, 1u << (t + 3), (uint32_t)E);
   }
 }
 
@@ -270,7 +290,8 @@ struct CalcConst {
 // CEM: the sum's carry renormalisation as an IMAD (Mn - cy 2^30) and the
 // cancellation offset as flo & 0xFFFFF000 inside the scale add: 1.2
 // instructions per MAC fewer, one FMA-pipe op fewer, ALU count unchanged.
-template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0), bool CEM = false>
+template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0), bool CEM = false,
+          bool PIX = false>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
@@ -280,7 +301,12 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   uint4 T;
   int32_t Ep;
   uint32_t mulp;
-  if constexpr (PBS) {
+  if constexpr (PIX) {
+    // aw + bw = address of entry (Ea + Eb, n = 0); n selects the odd entry
+    T = lds128(fmad(n, K.sixteen, aw + bw));
+    Ep = (int32_t)T.w;
+    mulp = T.z;
+  } else if constexpr (PBS) {
     // the table lookup depends only on Ea + Eb, so it overlaps the multiply
     T = PRE ? lds128(aw + bw) : K.prod2(Ea + Eb);
     Ep = Ea + Eb + (int32_t)n;                        // IADD3 (ALU / FMA balance)
@@ -292,7 +318,8 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   }
   // drop D = t + 2 + n bits of hi: hi * 2^(32 - D) splits into q (high) and the dropped bits (low, left-aligned)
   uint32_t qp, yp;
-  mulwide(hi, fmad(n, T.y, T.x), qp, yp);
+  if constexpr (PIX) mulwide(hi, T.x, qp, yp);
+  else mulwide(hi, fmad(n, T.y, T.x), qp, yp);
   uint32_t rp;
   asm("{\n\t.reg .u32 t;\n\t"
       "add.cc.u32 t, %1, 0xFFFFFFFF;\n\t"             // CF = (lo != 0)         (sticky)
