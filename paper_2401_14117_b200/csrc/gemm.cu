@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <initializer_list>
 #include <utility>
+#include <type_traits>
 #include "gemm.cuh"
 #include "internal.h"
 
@@ -38,17 +39,35 @@ struct Cfg {
   static constexpr int AQN = BM * BK / 4, BQN = BN * BK / 4;    // quads per tile
   static constexpr int AQ = (AQN + NTHR - 1) / NTHR;            // A quads per thread (last may idle)
   static constexpr int BQ = (BQN + NTHR - 1) / NTHR;
+  // MAC variants (see gemm.cuh): product table by Ea + Eb for 4 x 4 tiles (PBS),
+  // else the PIX table, with the signs folded in (PIXS)
+  static constexpr bool PBS = (PG_PROD_BY_SUM != 0) && (TM * TN >= 16);
+  static constexpr bool PIX = !PBS && (PG_PIX == 2 || (PG_PIX == 1 && MINB == 1));
+  static constexpr bool PIXS = PIX && PG_PIXS != 0;
+  // staged operand: {M, E, sigma, w}, or with PIXS only {M, w} (one LDS.64)
+  using SV = std::conditional_t<PIXS, uint2, uint4>;
   struct Smem {
-    uint4 a[2][BK][BM];
-    uint4 b[2][BK][BN];
+    SV a[2][BK][BM];
+    SV b[2][BK][BN];
 #if PG_CPASYNC
     uint32_t ra[BM * BK];                 // raw patterns of the next slab (cp.async target, by quad)
     uint32_t rb[BK * BN];
 #endif
-    uint4 tp[2 * TSIZE];                  // PIX: 2 entries per scale; else the first TSIZE
+    uint4 tp[3 * PIX_NE > TSIZE ? 3 * PIX_NE : TSIZE];   // PIX layout (up to 3 copies) or by scale
     uint4 tx[TSIZE];
   };
 };
+
+// staged-operand accessors ({M, E, sigma, w} or {M, w})
+template <class V> __device__ __forceinline__ V sv(const uint4& d);
+template <> __device__ __forceinline__ uint4 sv<uint4>(const uint4& d) { return d; }
+template <> __device__ __forceinline__ uint2 sv<uint2>(const uint4& d) { return make_uint2(d.x, d.w); }
+__device__ __forceinline__ int32_t sv_E(const uint4& v) { return (int32_t)v.y; }
+__device__ __forceinline__ int32_t sv_s(const uint4& v) { return (int32_t)v.z; }
+__device__ __forceinline__ uint32_t sv_w(const uint4& v) { return v.w; }
+__device__ __forceinline__ int32_t sv_E(const uint2&) { return 0; }     // unused by the PIXS MAC
+__device__ __forceinline__ int32_t sv_s(const uint2&) { return 1; }
+__device__ __forceinline__ uint32_t sv_w(const uint2& v) { return v.y; }
 
 // Generic per-operation MAC on patterns (the slow path; bit-identical to the
 // fast path by the contract).
@@ -123,10 +142,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, TM = C::TM, TN = C::TN, NTHR = C::NTHR;
   constexpr int AQ = C::AQ, BQ = C::BQ;
   // product table by Ea + Eb for the 16-warp (4 x 4) tiles, by Ep for the 32-warp (4 x 2) ones (r05p)
-  constexpr bool PBS = (PG_PROD_BY_SUM != 0) && (TM * TN >= 16);
+  constexpr bool PBS = C::PBS, PIX = C::PIX, PIXS = C::PIXS;
   constexpr bool CEM = PG_CECM == 2 || (PG_CECM == 1 && C::MINB == 1) || (PG_CECM == 3 && C::MINB > 1);
-  constexpr bool PIX = !PBS && (PG_PIX == 2 || (PG_PIX == 1 && C::MINB == 1));
   constexpr uint32_t WM = PIX ? 32u : 16u;   // staged .w = WM E (+ table base on the B side)
+  constexpr uint32_t SOFF = PIXS ? PIX_SOFF : 0u;   // + this for a negative operand
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(smem_raw);
 
@@ -150,10 +169,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
 
   const uint32_t flip = P.neg ? 1u : 0u;
   fill_tables<PBS, !PIX>(S.tp, S.tx, tid, NTHR);     // visible after the first __syncthreads_or
-  if constexpr (PIX) fill_prod_pix(S.tp, tid, NTHR);
+  if constexpr (PIX) fill_prod_pix<PIXS>(S.tp, tid, NTHR);
   MacConst K;
   K.one = (uint32_t)P.one; K.sixteen = 16u * K.one; K.m2p30 = 0xC0000000u * K.one;
-  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + (PIX ? 2 * TBIAS : TBIAS));
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + (PIX ? 2 * PIX_SB : TBIAS));
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + TBIAS) - 30u * 16u;   // indexed by Ex + 30
 
   // ---- accumulators -------------------------------------------------------
@@ -213,11 +232,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (!P.transa) {
         const int ar = e / (BK / 4), ak = (e % (BK / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = stage_decode<31, WM>(ra[h * 4 + q], 0u, sp);
+        for (int q = 0; q < 4; q++) S.a[buf][ak + q][ar] = sv<typename C::SV>(stage_decode<31, WM, SOFF>(ra[h * 4 + q], 0u, sp));
       } else {
         const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.a[buf][ak][ar + q] = stage_decode<31, WM>(ra[h * 4 + q], 0u, sp);
+        for (int q = 0; q < 4; q++) S.a[buf][ak][ar + q] = sv<typename C::SV>(stage_decode<31, WM, SOFF>(ra[h * 4 + q], 0u, sp));
       }
     }
 #pragma unroll
@@ -227,11 +246,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (!TRANS_B) {
         const int bk = e / (BN / 4), bc = (e % (BN / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = stage_decode<30, WM>(rb[h * 4 + q], flip, sp, K.tp0);
+        for (int q = 0; q < 4; q++) S.b[buf][bk][bc + q] = sv<typename C::SV>(stage_decode<30, WM, SOFF>(rb[h * 4 + q], flip, sp, K.tp0));
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
 #pragma unroll
-        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = stage_decode<30, WM>(rb[h * 4 + q], flip, sp, K.tp0);
+        for (int q = 0; q < 4; q++) S.b[buf][bk + q][bc] = sv<typename C::SV>(stage_decode<30, WM, SOFF>(rb[h * 4 + q], flip, sp, K.tp0));
       }
     }
     return sp;
@@ -286,14 +305,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         const int64_t av = P.k - (k0 + ak);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.a[buf][ak + q][ar] = stage_decode<31, WM>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+          S.a[buf][ak + q][ar] = sv<typename C::SV>(stage_decode<31, WM, SOFF>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp));
       } else {
         const int ak = e / (BM / 4), ar = (e % (BM / 4)) * 4;
         const bool rok = k0 + ak < P.k;
         const int64_t av = P.m - (row0 + ar);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.a[buf][ak][ar + q] = stage_decode<31, WM>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp);
+          S.a[buf][ak][ar + q] = sv<typename C::SV>(stage_decode<31, WM, SOFF>((rok && q < av) ? S.ra[e * 4 + q] : p32::ONE, 0u, sp));
       }
     }
 #pragma unroll
@@ -306,14 +325,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
         const int64_t av = P.n - (col0 + bc);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk][bc + q] = stage_decode<30, WM>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
+          S.b[buf][bk][bc + q] = sv<typename C::SV>(stage_decode<30, WM, SOFF>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0));
       } else {
         const int bc = e / (BK / 4), bk = (e % (BK / 4)) * 4;
         const bool rok = col0 + bc < P.n;
         const int64_t av = P.k - (k0 + bk);
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          S.b[buf][bk + q][bc] = stage_decode<30, WM>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0);
+          S.b[buf][bk + q][bc] = sv<typename C::SV>(stage_decode<30, WM, SOFF>((rok && q < av) ? S.rb[e * 4 + q] : p32::ONE, flip, sp, K.tp0));
       }
     }
     return sp;
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
       if (kmax == BK) {
 #pragma unroll (SYRK ? KK_UNROLL_SYRK : KK_UNROLL)
         for (int kk = 0; kk < BK; kk++) {
-          uint4 av[TM], bv[TN];
+          typename C::SV av[TM], bv[TN];
 #pragma unroll
           for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
 #pragma unroll
@@ -362,12 +381,12 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
-                                                      (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
+                                                                sv_E(bv[j]), sv_s(bv[j]), K, badacc, sv_w(av[i]), sv_w(bv[j]));
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
-          uint4 av[TM], bv[TN];
+          typename C::SV av[TM], bv[TN];
 #pragma unroll
           for (int i = 0; i < TM; i++) av[i] = S.a[cur][kk][ty * TM + i];
 #pragma unroll
@@ -376,8 +395,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX>(acc[i][j], av[i].x, (int32_t)av[i].y, (int32_t)av[i].z, bv[j].x,
-                                                      (int32_t)bv[j].y, (int32_t)bv[j].z, K, badacc, av[i].w, bv[j].w);
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
+                                                                sv_E(bv[j]), sv_s(bv[j]), K, badacc, sv_w(av[i]), sv_w(bv[j]));
         }
       }
     } else if (!bad) {

@@ -64,6 +64,12 @@ namespace pg {
 #ifndef PG_PIX                   // PIX product table (see fill_prod_pix): 1 one-CTA-per-SM tile, 2 every tile, 0 off
 #define PG_PIX 2
 #endif
+#ifndef PG_PIXS                  // signs folded into the PIX table (see fill_prod_pix): fewer instructions, but the
+#define PG_PIXS 0                // sign then waits for the lookup (r05y: C2 1242 -> 1215, C5 +5 ms) -> off
+#endif
+#ifndef PG_SUMADDR               // sum-table address as IMAD(flo, 16, 16 Ebg + base), one op fewer after the
+#define PG_SUMADDR 0             // leading-one search (r05z: C2 1242 = 1242, SYRK 1210 -> 1206) -> off
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -88,7 +94,7 @@ struct Params {
 // A side: significand hidden bit at 31.  B side: hidden bit at 30.
 // Staged element = {M, E, sigma (+1 / -1 as int), 0}.  Returns "special"
 // (zero, NaR, |E| > 53) through `special`.
-template <int HID, uint32_t WM = 16u>
+template <int HID, uint32_t WM = 16u, uint32_t SOFF = 0u>
 __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_t& special, uint32_t wbase = 0u) {
   const uint32_t s = (x >> 31) ^ flip;
   const uint32_t a = (x >> 31) ? (0u - x) : x;
@@ -101,7 +107,7 @@ __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_
   const uint32_t M = (0x80000000u | ((rest << 2) >> 1)) >> (31 - HID);
   special |= (uint32_t)((x << 1) == 0u) | (uint32_t)(E > E_STAGE_MAX) | (uint32_t)(E < -E_STAGE_MAX);
   // .w: 16 E + wbase, so that a product's table address is one add of the two operands' .w (PG_PRESCALED)
-  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, (uint32_t)E * WM + wbase);
+  return make_uint4(M, (uint32_t)E, s ? 0xFFFFFFFFu : 1u, (uint32_t)E * WM + wbase + (s ? SOFF : 0u));
 }
 
 // ---- accumulator <-> pattern (exact: the accumulator is on the lattice) ----
@@ -181,19 +187,28 @@ __device__ __forceinline__ void fill_tables(uint4* tp, uint4* tx, int tid, int n
   }
 }
 
-// PIX product table (the GEMM's one-CTA-per-SM tile): indexed by S = Ea + Eb
-// and the product's normalisation bit n, interleaved (entry 2 (S + TBIAS) + n),
-// so the address is one IMAD of n over the staged operands' prescaled sum
-// (.w = 32 E [+ base]), and the entry carries the multiplier that splits off
-// the dropped bits (n folded in), the renormalising power and Ep = S + n:
-//   { 2^(30 - n - t), 0, 2^(t + 3), S + n },  t = t(S + n)
+// PIX product table (GEMM / SYRK tiles): indexed by S = Ea + Eb and the
+// product's normalisation bit n, interleaved (entry 2 (S + PIX_SB) + n), so the
+// address is one IMAD of n over the staged operands' prescaled sum (.w = 32 E
+// [+ base]); the entry carries the multiplier that splits off the dropped bits
+// (n folded in), the product's sign, the renormalising power and Ep = S + n:
+//   { 2^(30 - n - t), sign, 2^(t + 3), S + n },  t = t(S + n)
+// With the signs folded in (PIXS) a negative operand adds PIX_SOFF bytes to its
+// .w, and three copies of the table (0, 1, 2 negative operands) give the sign
+// of the product from the lookup instead of an IMAD.  |Ea|, |Eb| <= 37 in the
+// fast MAC (staging), so S + n in [-74, 75] fits the 160 scales per copy.
+constexpr int PIX_SB = 80;                    // S bias: entry 2 (S + PIX_SB) + n
+constexpr int PIX_NE = 4 * PIX_SB;            // entries per copy (160 scales x 2)
+constexpr uint32_t PIX_SOFF = PIX_NE * 16u;   // bytes per copy (a negative operand's .w offset)
+template <bool SGN>
 __device__ __forceinline__ void fill_prod_pix(uint4* tp, int tid, int nthr) {
-  for (int i = tid; i < 2 * TSIZE; i += nthr) {
-    const uint32_t n = (uint32_t)i & 1u;
-    const int E = (i >> 1) - TBIAS + (int)n;
+  for (int i = tid; i < (SGN ? 3 : 1) * PIX_NE; i += nthr) {
+    const int cpy = i / PIX_NE, j = i % PIX_NE;
+    const uint32_t n = (uint32_t)j & 1u;
+    const int E = (j >> 1) - PIX_SB + (int)n;
     uint32_t t = (uint32_t)(E ^ (E >> 31)) >> 2;
     t = t < (uint32_t)T_FAST_MAX ? t : (uint32_t)T_FAST_MAX;
-    tp[i] = make_uint4(1u << (30 - n - t), 0u, 1u << (t + 3), (uint32_t)E);
+    tp[i] = make_uint4(1u << (30 - n - t), cpy == 1 ? 0xFFFFFFFFu : 1u, 1u << (t + 3), (uint32_t)E);
   }
 }
 
@@ -250,6 +265,10 @@ struct MacConst {
   __device__ __forceinline__ uint4 prod2(int32_t S) const { return lds128(fmad((uint32_t)S, sixteen, tp0)); }
   __device__ __forceinline__ uint4 sum(uint32_t Exi) const { return lds128(fmad(Exi, sixteen, tx0)); }
 #endif
+  // entry flo + Ebg: the 16 Ebg + base IMAD does not wait for the leading-one search
+  __device__ __forceinline__ uint4 sum2(uint32_t flo, uint32_t Ebg) const {
+    return lds128(fmad(flo, sixteen, fmad(Ebg, sixteen, tx0)));
+  }
 };
 
 // The same constants computed in registers (no shared-memory tables): used by
@@ -278,6 +297,7 @@ struct CalcConst {
     const uint32_t tc = fast ? t : (uint32_t)T_FAST_MAX;
     return make_uint4(fast ? (1u << (27 - t)) : 0u, 1u << (tc + 3), fast ? 0u : BAD_FLAG, (uint32_t)E);
   }
+  __device__ __forceinline__ uint4 sum2(uint32_t flo, uint32_t Ebg) const { return sum(flo + Ebg); }
 };
 
 // ---- the decoded-domain MAC -------------------------------------------------
@@ -291,7 +311,7 @@ struct CalcConst {
 // cancellation offset as flo & 0xFFFFF000 inside the scale add: 1.2
 // instructions per MAC fewer, one FMA-pipe op fewer, ALU count unchanged.
 template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0), bool CEM = false,
-          bool PIX = false>
+          bool PIX = false, bool PIXS = false>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
@@ -328,9 +348,9 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
       : "=r"(rp) : "r"(lo), "r"(yp | (qp & 1u)), "r"(qp));
   const uint32_t Mp = fmad(rp, mulp, 0u);             // hidden@30 (2^31 if rounding carried)
 #if PG_SIGN_LOP
-  const int32_t sp = (sa ^ sb) | 1;                   // +-1 x +-1 as one LOP3: (-1 = ~0, 1 = 1)
+  const int32_t sp = PIXS ? (int32_t)T.y : (sa ^ sb) | 1;   // +-1 x +-1 as one LOP3: (-1 = ~0, 1 = 1)
 #else
-  const int32_t sp = (int32_t)fmad((uint32_t)sa, (uint32_t)sb, 0u);
+  const int32_t sp = PIXS ? (int32_t)T.y : (int32_t)fmad((uint32_t)sa, (uint32_t)sb, 0u);
 #endif
 
   // -- sum: exact aligned add with jammed sticky, rounded once at f_s(Ex) --
@@ -362,12 +382,16 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   uint32_t flo;
   asm("bfind.u32 %0, %1;" : "=r"(flo) : "r"(x));             // leading one (0xFFFFFFFF if x == 0)
   const uint32_t xf = __funnelshift_r(0u, x, flo);            // fraction bits left-aligned (hidden dropped)
+#if PG_SUMADDR
+  const uint4 U = K.sum2(flo, (uint32_t)Ebg);                 // entry Ex + 30 = flo + Ebg
+#else
 #if PG_EXI_ALU
   const uint32_t Exi = flo + (uint32_t)Ebg;                   // Ex + 30
 #else
   const uint32_t Exi = fmad(flo, K.one, (uint32_t)Ebg);       // Ex + 30
 #endif
   const uint4 U = K.sum(Exi);
+#endif
   uint32_t qx, yx;
   mulwide(xf, U.x, qx, yx);                                   // f_s fraction bits | the rest, left-aligned
   uint32_t rx;
