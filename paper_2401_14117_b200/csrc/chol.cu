@@ -12,9 +12,12 @@ namespace pl {
 // operands, and each thread keeps its element decoded across the k loop.
 __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, int64_t b, int32_t* info,
                                                      int64_t row_base) {
-  __shared__ uint32_t colp[TB];          // column k patterns
-  __shared__ uint4 cola[TB];             // column k, A-format decode (hidden@31) + fast flag in .w
-  __shared__ uint4 colb[TB];             // column k, B-format decode (hidden@30) + fast flag in .w
+  // column k is published in buffer k & 1: warp k + 1 finishes its own step-k
+  // update, then factors column k + 1 before the barrier, so one barrier per
+  // column suffices (the buffer it overwrites was last read before the previous one)
+  __shared__ uint32_t colp[2][TB];       // column k patterns
+  __shared__ uint4 cola[2][TB];          // column k, A-format decode (hidden@31) + fast flag in .w
+  __shared__ uint4 colb[2][TB];          // column k, B-format decode (hidden@30) + fast flag in .w
   __shared__ int fail;
   if (*info != 0) return;                                  // an earlier block failed: stop
   const int j = threadIdx.x >> 5, i = threadIdx.x & 31;    // column (warp), row (lane)
@@ -22,47 +25,51 @@ __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, i
   LaneVal v;
   lv_load(v, in ? A[i * lda + j] : 0u);
   if (threadIdx.x == 0) fail = 0;
-  __syncthreads();
-  int k = 0;
-  for (; k < b; k++) {
-    if (j == k) {                                          // warp k: pivot, then the column's divisions
-      uint32_t d = 0u;
-      if (i == k) {
+  // warp j factors its column (pivot sqrt, then the divisions) and publishes it
+  auto factor = [&](int k) {
+    uint32_t d = 0u;
+    if (i == k) {
+      d = lv_pattern(v);
+      if ((int32_t)d > 0) {
+        lv_load(v, p32::sqrt(d));
         d = lv_pattern(v);
-        if ((int32_t)d > 0) {
-          lv_load(v, p32::sqrt(d));
-          d = lv_pattern(v);
-        }
-      }
-      d = __shfl_sync(0xFFFFFFFFu, d, k);
-      if ((int32_t)d <= 0) {                               // zero, negative or NaR pivot
-        if (i == k) { fail = 1; *info = (int32_t)(row_base + k + 1); }
-      } else if (in && i > k) {
-        // decoded division by the shared divisor (one reciprocal), generic outside its range
-        pg::Acc dv;
-        const bool dok = pg::acc_decode(d, dv) && dv.E <= 37 && dv.E >= -37;
-        bool done = false;
-        if (dok && v.dec) {
-          done = pg::acc_div(v.a, dv.M, dv.E, dv.sg, __drcp_rn((double)dv.M) * 4294967296.0, pg::CalcConst());
-          if (done && !(v.a.E <= 75 && v.a.E >= -75) && v.a.E > pg::E_ZERO_LIMIT) {
-            v.pat = pg::acc_encode(v.a);
-            v.dec = false;
-          }
-        }
-        if (!done) lv_load(v, div(lv_pattern(v), d));
-        const uint32_t x = lv_pattern(v);
-        colp[i] = x;
-        uint4 ad;
-        cola[i] = fast_a(x, ad) ? make_uint4(ad.x, ad.y, ad.z, 1u) : make_uint4(0u, 0u, 0u, 0u);
-        colb[i] = lv_operand(v) ? make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)v.a.sg, 1u) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    __syncthreads();
+    d = __shfl_sync(0xFFFFFFFFu, d, k);
+    if ((int32_t)d <= 0) {                               // zero, negative or NaR pivot
+      if (i == k) { fail = 1; *info = (int32_t)(row_base + k + 1); }
+    } else if (in && i > k) {
+      // decoded division by the shared divisor (one reciprocal), generic outside its range
+      pg::Acc dv;
+      const bool dok = pg::acc_decode(d, dv) && dv.E <= 37 && dv.E >= -37;
+      bool done = false;
+      if (dok && v.dec) {
+        done = pg::acc_div(v.a, dv.M, dv.E, dv.sg, __drcp_rn((double)dv.M) * 4294967296.0, pg::CalcConst());
+        if (done && !(v.a.E <= 75 && v.a.E >= -75) && v.a.E > pg::E_ZERO_LIMIT) {
+          v.pat = pg::acc_encode(v.a);
+          v.dec = false;
+        }
+      }
+      if (!done) lv_load(v, div(lv_pattern(v), d));
+      const uint32_t x = lv_pattern(v);
+      const int q = k & 1;
+      colp[q][i] = x;
+      uint4 ad;
+      cola[q][i] = fast_a(x, ad) ? make_uint4(ad.x, ad.y, ad.z, 1u) : make_uint4(0u, 0u, 0u, 0u);
+      colb[q][i] = lv_operand(v) ? make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)v.a.sg, 1u) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  __syncthreads();                                         // fail = 0 visible
+  if (j == 0 && b > 0) factor(0);
+  __syncthreads();
+  for (int k = 0; k < b; k++) {
     if (fail) break;
+    const int q = k & 1;
     if (in && j > k) {
-      const uint4 ad = cola[i], bd = colb[j];
-      lv_fms(v, colp[i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, colp[j]);
+      const uint4 ad = cola[q][i], bd = colb[q][j];
+      lv_fms(v, colp[q][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, colp[q][j]);
     }
+    if (j == k + 1 && j < b) factor(k + 1);
     __syncthreads();
   }
   if (in) A[i * lda + j] = lv_pattern(v);
