@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
   // product table by Ea + Eb for the 16-warp (4 x 4) tiles, by Ep for the 32-warp (4 x 2) ones (r05p)
   constexpr bool PBS = C::PBS, PIX = C::PIX, PIXS = C::PIXS;
   constexpr bool CEM = PG_CECM == 2 || (PG_CECM == 1 && C::MINB == 1) || (PG_CECM == 3 && C::MINB > 1);
+  constexpr bool MSL = PG_MSM_SEL == 2 || (PG_MSM_SEL == 1 && C::MINB == 1);
   constexpr uint32_t WM = PIX ? 32u : 16u;   // staged .w = WM E (+ table base on the B side)
   constexpr uint32_t SOFF = PIXS ? PIX_SOFF : 0u;   // + this for a negative operand
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS, MSL>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
                                                                 sv_E(bv[j]), sv_s(bv[j]), K, badacc, sv_w(av[i]), sv_w(bv[j]));
         }
       } else {
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm(Params P) {
           for (int i = 0; i < TM; i++)
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
+              mac<MacConst, false, PG_PRESCALED != 0, PBS, CEM, PIX, PIXS, MSL>(acc[i][j], av[i].x, sv_E(av[i]), sv_s(av[i]), bv[j].x,
                                                                 sv_E(bv[j]), sv_s(bv[j]), K, badacc, sv_w(av[i]), sv_w(bv[j]));
         }
       }

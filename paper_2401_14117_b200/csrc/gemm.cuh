@@ -70,6 +70,12 @@ namespace pg {
 #ifndef PG_SUMADDR               // sum-table address as IMAD(flo, 16, 16 Ebg + base), one op fewer after the
 #define PG_SUMADDR 0             // leading-one search (r05z: C2 1242 = 1242, SYRK 1210 -> 1206) -> off
 #endif
+#ifndef PG_MSM_SEL               // the smaller operand by SEL (beside the larger) instead of Mp + Mc - Mbg: 0 off,
+#define PG_MSM_SEL 1             // 1 in the one-CTA-per-SM tile, 2 every tile (r06c: C2 1242 -> 1244, 2-CTA SYRK
+#endif                           // 1210 -> 1204)
+#ifndef PG_HI_FMA                // 1: product normalisation bit, 2: sum carry as IMAD.HI (FMA pipe) instead of SHF
+#define PG_HI_FMA 0
+#endif
 #ifndef PG_PROD_BY_SUM
 #define PG_PROD_BY_SUM 1
 #endif
@@ -220,6 +226,14 @@ __device__ __forceinline__ uint32_t fmad(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// x >> (32 - log2 m) as IMAD.HI on the FMA pipe (m from a kernel parameter, so
+// ptxas cannot turn it back into a shift on the ALU pipe)
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t m) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(m));
+  return d;
+}
+
 // 32 x 32 -> 64-bit product as (hi, lo): one IMAD.WIDE.U32
 __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
   asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%1, %0}, w;\n\t}" : "=r"(hi), "=r"(lo) : "r"(a), "r"(b));
@@ -311,13 +325,17 @@ struct CalcConst {
 // cancellation offset as flo & 0xFFFFF000 inside the scale add: 1.2
 // instructions per MAC fewer, one FMA-pipe op fewer, ALU count unchanged.
 template <class Tab, bool TRACK = true, bool PRE = false, bool PBS = (PG_PROD_BY_SUM != 0), bool CEM = false,
-          bool PIX = false, bool PIXS = false>
+          bool PIX = false, bool PIXS = false, bool MSL = false>
 __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa, uint32_t Mb, int32_t Eb, int32_t sb,
                                     const Tab& K, uint32_t& badacc, uint32_t aw = 0u, uint32_t bw = 0u) {
   // -- product: exact 56-bit product, rounded once at f_s(Ep) -------------
   uint32_t hi, lo;
   mulwide(Ma, Mb, hi, lo);                            // hi in [2^29, 2^31)
+#if PG_HI_FMA & 1
+  const uint32_t n = mulhi(hi, 4u * K.one);           // hi >> 30 on the FMA pipe
+#else
   const uint32_t n = hi >> 30;
+#endif
   uint4 T;
   int32_t Ep;
   uint32_t mulp;
@@ -359,7 +377,8 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
   const long long kc = (long long)(((unsigned long long)(uint32_t)c.E << 32) | c.M);
   const bool pbig = kp > kc;
   const uint32_t Mbg = pbig ? Mp : c.M;
-  const uint32_t Msm = Mp + c.M - Mbg;                // the other one
+  // the other one: a SEL beside Mbg's (MSL), or Mp + Mc - Mbg
+  const uint32_t Msm = MSL ? (pbig ? c.M : Mp) : Mp + c.M - Mbg;
   const int32_t sbg = pbig ? sp : c.sg;
   const int32_t Ebg = max(Ep, c.E);
 #if PG_AD_SAD
@@ -400,7 +419,11 @@ __device__ __forceinline__ void mac(Acc& c, uint32_t Ma, int32_t Ea, int32_t sa,
       "addc.u32 %0, %2, %3;\n\t}"                      // + hidden bit + round up
       : "=r"(rx) : "r"(yx | (qx & 1u)), "r"(qx), "r"(U.x));
   const uint32_t Mn = fmad(rx, U.y, 0u);                      // hidden@30, or 2^31 on carry
+#if PG_HI_FMA & 2
+  const uint32_t cy = mulhi(Mn, 2u * K.one);                  // Mn >> 31 on the FMA pipe
+#else
   const uint32_t cy = Mn >> 31;
+#endif
   if constexpr (CEM) c.M = fmad(cy, K.m2p30, Mn);            // 2^31 -> 2^30 (IMAD instead of a shift)
   else c.M = Mn >> cy;
   // exact cancellation (x == 0, flo = -1): scale pushed far below any product,
