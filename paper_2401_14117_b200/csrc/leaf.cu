@@ -407,11 +407,16 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     return e ? atoi(e) : 0;
   }();
   const bool wide = force ? force > 16 : allow_coop;
-  static const int side_ctas = [] {              // side-stream leaf CTAs (1024 threads each)
+  static const int side_env = [] {               // side-stream leaf CTAs (1024 threads each); 0: auto
     const char* e = getenv("POSIT_SIDE_LEAF_CTAS");
-    const int v = e ? atoi(e) : 16;
-    return v > 0 ? v : 16;
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 0;
   }();
+  // auto: 1024 rows per CTA, 8 to 16 CTAs (fewer CTAs leave more SMs to the
+  // concurrent trailing update; r06e: C5 343.1 -> 342.2 ms with 8, and 16 at
+  // m = 16384, where 8 would not fit the leaf in shared memory)
+  const int64_t side_auto = (m + 1023) / 1024 < 8 ? 8 : ((m + 1023) / 1024 > 16 ? 16 : (m + 1023) / 1024);
+  const int side_ctas = side_env > 0 ? side_env : (int)side_auto;
   int nctas = wide ? nsm : (nsm < side_ctas ? nsm : side_ctas);
   int nthr = wide ? COOP_THREADS : 1024;
   if (force > 0 && force != 16 && force != 148) { nctas = force < nsm ? force : nsm; nthr = COOP_THREADS; }

@@ -1,4 +1,6 @@
-"""C3 Cholesky timing only (median of 3), for A/B runs of panel-side variants."""
+"""C3 Cholesky / C5 LU (median of 3) or C4 LU (median of 2) timing only, for A/B runs of panel-side variants:
+    python tools/time_chol.py [chol|lu|c4]
+"""
 import json
 import os
 import sys
@@ -12,5 +14,7 @@ from time_lapack import chol, lu  # noqa: E402
 which = sys.argv[1] if len(sys.argv) > 1 else "chol"
 if which == "chol":
     chol("C3 " + os.environ.get("TAG", ""), SI.config3(), SI.C3_NB, reps=3)
+elif which == "c4":
+    lu("C4 " + os.environ.get("TAG", ""), SI.config4(), SI.C4_NB, reps=2)
 else:
     lu("C5 s=0 " + os.environ.get("TAG", ""), SI.config5(0), SI.C5_NB, reps=3)
