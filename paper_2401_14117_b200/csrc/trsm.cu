@@ -277,6 +277,23 @@ __global__ void __launch_bounds__(1024) k_trsm_rltn_blk(const uint32_t* L, int64
 // still arrive one at a time in ascending k (Q6).
 constexpr int FR_NMAX = 256;
 
+// PG_RLTN_PIX: the update loop's MAC on the PIX product table (see gemm.cuh):
+// staged L and block values carry .w = 32 E (+ the table base on the B side);
+// the slow path then takes L's patterns from global memory and the block's
+// final patterns from the row tile.
+#ifndef PG_RLTN_PIX
+#define PG_RLTN_PIX 1
+#endif
+#if PG_RLTN_PIX
+#define FR_LW(x, E) ((uint32_t)(E) * 32u)
+#define FR_BW(x, E) ((uint32_t)(E) * 32u + tpx0)
+#define FR_LPAT(col, k) L[(int64_t)(col) * ldl + c0 + (k)]
+#else
+#define FR_LW(x, E) (x)
+#define FR_BW(x, E) (x)
+#define FR_LPAT(col, k) S.ld[k][col].w
+#endif
+
 template <int W, int FR_ROWS>
 struct FrSmem {
   uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
@@ -290,6 +307,9 @@ struct FrSmem {
   int rowfast[FR_ROWS];                       // row r's block-J values all fast-path operands
   uint4 tp[pg::TSIZE];                        // the MAC's per-scale constant tables
   uint4 tx[pg::TSIZE];
+#if PG_RLTN_PIX
+  uint4 tpx[pg::PIX_NE];                      // the PIX product table of the update loop
+#endif
 };
 
 template <int W, int FR_ROWS>
@@ -310,6 +330,10 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
   K.one = (uint32_t)one; K.sixteen = 16u * K.one;
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
+#if PG_RLTN_PIX
+  pg::fill_prod_pix<false>(S.tpx, tid, NT);
+  const uint32_t tpx0 = (uint32_t)__cvta_generic_to_shared(S.tpx + 2 * pg::PIX_SB);
+#endif
   for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
     const int rr = e / (int)n, cc = e % (int)n;
     S.b[rr][cc] = rr < rows ? B[(r0 + rr) * ldb + cc] : 0u;
@@ -348,7 +372,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
         for (int k = 0; k < W; k++) {
           uint4 d;
           const bool fk = fast_a(xs[k], d);
-          S.ld[k][j] = make_uint4(d.x, d.y, d.z, xs[k]);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, FR_LW(xs[k], d.y));
           f &= (int)fk;
         }
       } else {
@@ -356,7 +380,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
           const uint32_t x = L[(int64_t)j * ldl + c0 + k];
           uint4 d;
           const bool fk = fast_a(x, d);
-          S.ld[k][j] = make_uint4(d.x, d.y, d.z, x);
+          S.ld[k][j] = make_uint4(d.x, d.y, d.z, FR_LW(x, d.y));
           f &= (int)fk;
         }
       }
@@ -406,7 +430,8 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
       if (live) {
         const uint32_t x = lv_pattern(v);
         S.b[r][c0 + c] = x;
-        S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), x);   // sign pre-negated: c (-) a b
+        // sign pre-negated: c (-) a b
+        S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), FR_BW(x, (uint32_t)v.a.E));
       }
       if (c == 0) S.rowfast[r] = allf ? 1 : 0;
     }
@@ -440,7 +465,12 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
 #pragma unroll
             for (int u = 0; u < G; u++) {
               const uint4 ad = S.ld[k][min(col0 + u * W, (int)n - 1)];
+#if PG_RLTN_PIX
+              pg::mac<pg::MacConst, true, false, false, false, true>(a[u], ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x,
+                                                                      (int32_t)bd.y, (int32_t)bd.z, K, bad, ad.w, bd.w);
+#else
               pg::mac(a[u], ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x, (int32_t)bd.y, (int32_t)bd.z, K, bad);
+#endif
             }
           }
 #pragma unroll
@@ -452,7 +482,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
             const int col = col0 + u * W;
             if (col >= (int)n) break;
             uint32_t y = x[u];
-            for (int k = 0; k < jb; k++) y = sub(y, mul(S.ld[k][col].w, S.bop[r][k].w));
+            for (int k = 0; k < jb; k++) y = sub(y, mul(FR_LPAT(col, k), S.b[r][c0 + k]));
             S.b[r][col] = y;
           }
         }
