@@ -148,6 +148,34 @@ def test_gemm_fast_path_range_boundaries(cuda_ok, ea, ec):
     assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
 
 
+@pytest.mark.parametrize("ea", [37, -37, 35])
+@pytest.mark.parametrize("m,n", [(300, 520), (520, 300), (330, 330)])
+def test_gemm_tiled_product_table_edges(cuda_ok, ea, m, n):
+    # shapes above the tiny-kernel cut-off, so the tiled kernels run: operand
+    # scales at the staging limit (|Ea|, |Eb| = 37 -> Ea + Eb + n at the ends of
+    # the PIX product table), both signs, accumulators of either sign and scale
+    rng = np.random.default_rng(abs(ea) * 7 + m)
+    k = 48
+    A = np.ldexp(rng.uniform(1.0, 2.0, (m, k)) * rng.choice([-1.0, 1.0], (m, k)), ea + rng.integers(-1, 1, (m, k)))
+    B = np.ldexp(rng.uniform(1.0, 2.0, (k, n)) * rng.choice([-1.0, 1.0], (k, n)), ea + rng.integers(-1, 1, (k, n)))
+    C = np.ldexp(rng.standard_normal((m, n)), 2 * ea + rng.integers(-2, 3, (m, n)))
+    A, B, C = _pats(A), _pats(B), _pats(C)
+    assert mismatch(_gpu_gemm(A, B, C), O.gemm(A, B, C)) == 0
+
+
+@pytest.mark.parametrize("ea", [37, -37])
+def test_syrk_tiled_product_table_edges(cuda_ok, ea):
+    import paper_2401_14117_b200 as PB
+    rng = np.random.default_rng(abs(ea) + 11)
+    n, k = 330, 40
+    A = np.ldexp(rng.uniform(1.0, 2.0, (n, k)) * rng.choice([-1.0, 1.0], (n, k)), ea + rng.integers(-1, 1, (n, k)))
+    C = np.ldexp(rng.standard_normal((n, n)), 2 * ea)
+    A, C = _pats(A), _pats(C)
+    dC = to_dev(C)
+    PB.posit_syrk(to_dev(A), dC)
+    assert mismatch(to_host(dC), O.syrk_lower(A, C)) == 0
+
+
 @pytest.mark.parametrize("transa,transb", [("N", "N"), ("T", "N"), ("N", "T")])
 @pytest.mark.parametrize("alpha,beta", [(2.5, 0.75), (-3.0, 1.0), (1.0, 0.0), (0.1, -2.0), (-1.0, 1.0)])
 def test_gemm_eq2_general_alpha_beta(cuda_ok, transa, transb, alpha, beta):
