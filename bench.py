@@ -2,25 +2,35 @@
 """Benchmark of the Posit(32,2) hot path on B200 (driver contract: one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload gemm|lu|cholesky]
-                    [--impl ours|reference]
+                    [--impl ours|reference] [--force-dist] [--no-factor-keys]
 
 Default workload = BASELINE.json configs[1], the metric's headline config:
 Posit(32,2) GEMM C <- C - A.B, m = n = k = 4096, A, B, C ~ N(0,1) binary64 from
 seed 1 rounded to posit32 (row-major uint32 patterns), every multiply and add
 correctly rounded, ascending-k order.  A "step" is one such GEMM on fresh C
 (C is restored from a resident copy inside the step: 64 MiB device copy).
-value = posit Gflop/s = 2 m n k / step time, summed over ranks (each rank runs
-its own configs[1] problem: weak scaling, no data-path collective).
+At N = 1 it is the single-GPU C ABI call.  Under torchrun (N > 1, or with
+--force-dist at N = 1) it is ONE 4096^3 problem split by column slabs of B and
+C over the ranks, A broadcast from rank 0 over NCCL inside every step
+(strong scaling).  value = 2 m n k / max-over-ranks step time.
 
---workload lu        configs[3] at N=1 (n = 16384, nb = 256), 2n^3/3 flops
---workload cholesky  configs[2] (n = 8192, nb = 256), n^3/3 flops
---impl reference     the CPU oracle (oracle/), on this box's host cores, on a
-                     bounded sample of the same workload (rank 0 only).
+Every run also carries the metric's other two rows at the same N:
+  lu_c4    configs[3]: LU n = 16384, nb = 256 (2n^3/3 flops; getrf_dist over
+           NCCL when distributed, else posit_getrf)
+  chol_c3  configs[2]: Cholesky n = 8192, nb = 256 (n^3/3; potrf_dist / posit_potrf)
+each with its own clocks and launches, and every output word of C2, C4 and C3
+compared with the committed oracle digests (tests/golden/config_digests,
+written by tools/oracle_digests.py): "parity" keys.
 
-Extra keys: roofline (issue-bound integer ALU roofline of the GEMM kernel),
-cpu_baseline (oracle sample), e2e (posit_gemm_host with pinned host buffers,
-copies inside the timed region), clocks (nvidia-smi during the timed region),
-gpu_launches (our kernel launches in the timed region).
+--workload lu|cholesky  make configs[3] / configs[2] the main line
+--impl reference        the CPU oracle (oracle/), on this box's host cores, on a
+                        bounded sample of the same workload (rank 0 only).
+
+Extra keys: roofline (issue-bound integer ALU roofline of the GEMM kernel,
+instruction count bound to the kernel's SASS hash), cpu_baseline (oracle
+sample), e2e (posit_gemm_host with pinned host buffers, copies inside the timed
+region), clocks (nvidia-smi during the timed region), gpu_launches (our kernel
+launches in the timed region).
 """
 from __future__ import annotations
 
@@ -40,7 +50,6 @@ import numpy as np  # noqa: E402
 METRIC = "Posit(32,2) Gflop/s (GEMM 2mnk; LU 2n^3/3; Cholesky n^3/3)"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_PATH = os.path.join(ROOT, "profiles", "gemm_kernel_profile.json")
-N_SM = 148
 LANES_PER_SM = 128        # 4 SMSPs x 1 warp-instruction (32 lanes) per clock: the issue limit
 
 
@@ -175,162 +184,214 @@ def run_reference(args):
     cb["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gflop/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "posit32 (int32 ALU)", "data": "synthetic",
-            "config": _config(args), "cpu_baseline": cb,
+            "scaling": "strong" if args.gpus > 1 or args.workload != "gemm" else "weak", "vs_baseline": None,
+            "dtype": "posit32 (int32 ALU)", "data": "synthetic",
+            "config": _config(args, args.gpus, args.gpus > 1), "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _config(args):
+def _config(args, world=1, dist_on=False):
     if args.workload == "gemm":
         return {"workload": "configs[1]: Posit(32,2) GEMM C -= A.B, m=n=k=4096, N(0,1) seed 1, row-major",
                 "m": 4096, "n": 4096, "k": 4096, "order": "ascending-k, per-op RNE, no quire",
-                "l2": "inputs (3 x 64 MiB) larger than the 126 MB L2", "parallelism": f"replica x{args.gpus}"}
+                "l2": "inputs (3 x 64 MiB) larger than the 126 MB L2",
+                "parallelism": (f"C split by column slabs over {world} rank(s), A broadcast over NCCL each step "
+                                "(one problem, strong scaling)" if dist_on else "single GPU")}
     if args.workload == "lu":
-        return {"workload": "configs[3] at 1 GPU: Posit(32,2) LU with partial pivoting, n=16384, nb=256, U[-1,1) seed 3",
+        return {"workload": "configs[3]: Posit(32,2) LU with partial pivoting, n=16384, nb=256, U[-1,1) seed 3",
                 "n": 16384, "nb": 256, "l2": "matrix 1 GiB > L2",
-                "parallelism": (f"1x{args.gpus} column-block-cyclic, NCCL panel broadcast" if args.gpus > 1 else "single GPU")}
+                "parallelism": (f"1x{world} column-block-cyclic, NCCL panel broadcast" if dist_on else "single GPU")}
     return {"workload": "configs[2]: Posit(32,2) Cholesky, n=8192, nb=256, A = G G^T/n + I seed 2",
             "n": 8192, "nb": 256, "l2": "matrix 256 MiB > L2",
-            "parallelism": (f"1x{args.gpus} column-block-cyclic, NCCL panel broadcast" if args.gpus > 1 else "single GPU")}
+            "parallelism": (f"1x{world} column-block-cyclic, NCCL panel broadcast" if dist_on else "single GPU")}
 
 
 # ---------------------------------------------------------------------- our arm
-def run_ours(args):
+DIGESTS = os.path.join(ROOT, "tests", "golden", "config_digests")
+
+
+def parity_vs_oracle(cfg, M, ipiv=None, info=None):
+    """Every output word of this run against the committed oracle digests
+    (tests/golden/config_digests/<cfg>.json, written by tools/oracle_digests.py
+    from the CPU oracle alone): per-row SHA-256 + whole-output SHA-256."""
+    import hashlib
+    ref = _load_json(os.path.join(DIGESTS, f"{cfg}.json"))
+    M = np.ascontiguousarray(M).view(np.uint32)
+    h = hashlib.sha256(M.tobytes())
+    if ipiv is not None:
+        h.update(np.ascontiguousarray(ipiv, np.int32).tobytes())
+    if info is not None:
+        h.update(np.array([info], np.int32).tobytes())
+    out = {"config": cfg, "words": int(M.size), "gpu_sha": h.hexdigest()}
+    if ref is None:
+        out.update({"oracle_sha": None, "mismatches": None, "note": "no oracle digest committed for this config"})
+        return out
+    rows = [hashlib.sha256(M[i].tobytes()).hexdigest()[:16] for i in range(M.shape[0])]
+    bad = [i for i, (g, o) in enumerate(zip(rows, ref["row_digests"])) if g != o]
+    out.update({"oracle_sha": ref["output_sha256"], "mismatched_rows": len(bad),
+                "first_bad_row": bad[0] if bad else None,
+                "mismatches": 0 if (not bad and out["gpu_sha"] == ref["output_sha256"]) else max(1, len(bad)),
+                "oracle_version": ref["oracle_sha256"][:16]})
+    return out
+
+
+def _timed(step, steps, warmup, stream, barrier, local, dist_on, PB):
+    """W untimed steps; K steps between barrier + synchronize, CUDA events on
+    the launching stream, nvidia-smi clocks during the timed region; returns
+    (max-over-ranks ms per step, clocks, our kernel launches)."""
     import torch
     import torch.distributed as dist
-    import paper_2401_14117_b200 as PB
-    import synthetic_inputs as SI
-
-    rank, world, local = _env_rank()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- inputs resident in HBM (converted by our posit_from_f64 kernel) ----
-    if args.workload == "gemm":
-        m = n = k = 4096
-        A64, B64, C64 = SI.config2()
-        dA = PB.posit_from_f64(torch.from_numpy(A64).to(dev))
-        dB = PB.posit_from_f64(torch.from_numpy(B64).to(dev))
-        dC0 = PB.posit_from_f64(torch.from_numpy(C64).to(dev))
-        dC = dC0.clone()
-        flops = 2.0 * m * n * k
-
-        def step():
-            dC.copy_(dC0)
-            PB.posit_gemm(dA, dB, dC)
-    elif args.workload == "lu":
-        nn = SI.C4_N
-        full = PB.posit_from_f64(torch.from_numpy(SI.config4()).to(dev))
-        ipiv = torch.zeros(nn, dtype=torch.int32, device=dev)
-        info = torch.zeros(1, dtype=torch.int32, device=dev)
-        flops = 2.0 * nn ** 3 / 3
-        if world > 1:
-            # configs[3]: ONE n = 16384 LU shared by all ranks (1 x P column-block-cyclic, NCCL panel broadcast)
-            from paper_2401_14117_b200.dist import BlockCyclic1D, getrf_dist
-            desc = BlockCyclic1D(nn, SI.C4_NB, world, rank)
-            dA0 = desc.scatter(full)
-            del full
-            dA = dA0.clone()
-
-            def step():
-                dA.copy_(dA0)
-                getrf_dist(dA, desc, ipiv, info)
-        else:
-            dA0 = full
-            dA = dA0.clone()
-
-            def step():
-                dA.copy_(dA0)
-                PB.posit_getrf(dA, ipiv, info, nb=SI.C4_NB)
-    else:
-        nn = SI.C3_N
-        full = PB.posit_from_f64(torch.from_numpy(SI.config3()).to(dev))
-        info = torch.zeros(1, dtype=torch.int32, device=dev)
-        flops = nn ** 3 / 3.0
-        if world > 1:
-            # configs[2]: ONE n = 8192 Cholesky shared by all ranks (1 x P column-block-cyclic)
-            from paper_2401_14117_b200.dist import BlockCyclic1D, potrf_dist
-            desc = BlockCyclic1D(nn, SI.C3_NB, world, rank)
-            dA0 = desc.scatter(full)
-            del full
-            dA = dA0.clone()
-
-            def step():
-                dA.copy_(dA0)
-                potrf_dist(dA, desc, info)
-        else:
-            dA0 = full
-            dA = dA0.clone()
-
-            def step():
-                dA.copy_(dA0)
-                PB.posit_potrf(dA, info, nb=SI.C3_NB)
-    # whole-job work: the GEMM runs one problem per rank (weak scaling); LU and
-    # Cholesky are one problem distributed over all ranks (strong scaling)
-    strong = args.workload in ("lu", "cholesky") and world > 1
-    job_flops = flops if strong else world * flops
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     barrier()
-
-    # ---- timed region -------------------------------------------------------
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         launches0 = PB.posit_kernel_launches()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         ev1.record(stream)
         launches = PB.posit_kernel_launches() - launches0
         barrier()
-    t_ms = ev0.elapsed_time(ev1)
-    t_tensor = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
-    t_max = float(t_tensor.item())
-    ms_per_step = t_max / args.steps
-    value = job_flops / (ms_per_step * 1e-3) / 1e9
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=torch.device("cuda", local))
+    if dist_on:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()) / steps, clk.summary(), launches
+
+
+def _gather_cols(local, desc, world):
+    """Full matrix from every rank's column blocks (rank 0 result; outside timing)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return desc.gather([local]) if desc is not None else local
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local.contiguous())
+    return desc.gather(parts)
+
+
+def factor_key(kind, args, dev, stream, barrier, local, rank, world, dist_on, PB):
+    """lu_c4 (configs[3], n = 16384, nb = 256) or chol_c3 (configs[2], n = 8192,
+    nb = 256): the factorisation on all ranks (1 x P column-block-cyclic over
+    NCCL when distributed, else the single-GPU C ABI), timed like the main line,
+    with its own clocks and a word-by-word parity check of the factors."""
+    import torch
+    import synthetic_inputs as SI
+    from paper_2401_14117_b200.dist import BlockCyclic1D, getrf_dist, potrf_dist
+    lu = kind == "lu"
+    nn, nb = (SI.C4_N, SI.C4_NB) if lu else (SI.C3_N, SI.C3_NB)
+    full = PB.posit_from_f64(torch.from_numpy(SI.config4() if lu else SI.config3()).to(dev))
+    ipiv = torch.zeros(nn, dtype=torch.int32, device=dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    desc = BlockCyclic1D(nn, nb, world, rank) if dist_on else None
+    dA0 = desc.scatter(full) if dist_on else full
+    del full
+    dA = dA0.clone()
+    if lu:
+        def step():
+            dA.copy_(dA0)
+            if dist_on:
+                getrf_dist(dA, desc, ipiv, info)
+            else:
+                PB.posit_getrf(dA, ipiv, info, nb=nb)
+    else:
+        def step():
+            dA.copy_(dA0)
+            if dist_on:
+                potrf_dist(dA, desc, info)
+            else:
+                PB.posit_potrf(dA, info, nb=nb)
+    steps, warmup = (args.factor_steps, 1) if lu else (max(3, args.factor_steps), 3)
+    ms, clocks, launches = _timed(step, steps, warmup, stream, barrier, local, dist_on, PB)
+    flops = 2.0 * nn ** 3 / 3 if lu else nn ** 3 / 3.0
+    M = _gather_cols(dA, desc, world)
+    out = None
+    if rank == 0:
+        cfg = "C4" if lu else "C3"
+        out = {"workload": ("configs[3]: LU with partial pivoting n=16384 nb=256 U[-1,1) seed 3" if lu else
+                            "configs[2]: Cholesky n=8192 nb=256 A = G G^T/n + I seed 2"),
+               "value": flops / (ms * 1e-3) / 1e9, "unit": "Gflop/s", "ms_per_step": ms, "steps": steps,
+               "warmup": warmup, "flops": flops,
+               "parallelism": (f"1x{world} column-block-cyclic, NCCL panel broadcast, lookahead" if dist_on
+                               else "single GPU (posit_getrf / posit_potrf, lookahead)"),
+               "scaling": "strong", "clocks": clocks, "gpu_launches": launches,
+               "info": int(info.cpu()[0]),
+               "parity": parity_vs_oracle(cfg, M.cpu().numpy(), ipiv.cpu().numpy() if lu else None,
+                                          int(info.cpu()[0]))}
+    del dA, dA0, M
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2401_14117_b200 as PB
+    import synthetic_inputs as SI
+    from paper_2401_14117_b200.dist import col_slab, gemm_colsplit
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dist_on = world > 1 or args.force_dist
+    if dist_on:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist_on:
+            dist.barrier()
+        torch.cuda.synchronize()
 
     line = None
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
-                "vs_baseline": None, "dtype": "posit32 (int32 ALU; every mul/add correctly rounded)",
-                "data": "synthetic (seeded numpy PCG64, BASELINE recipe)", "config": _config(args),
-                "clocks": clk.summary(), "gpu_launches": launches,
-                "paper_context": {"gemm_gflops_rtx4090_n8000": 181.4, "gemm_gflops_agilex_n8000": 202.7,
-                                  "lu_gflops_rx7900_n8000": 13.4, "source": "PAPER.md:403,432,542"}}
-
-    # ---- energy efficiency (Table PowerE analog): NVML board power of
-    # this GPU during the timed region, not the paper's AC wall power
-    if rank == 0:
-        pw = line["clocks"].get("power_w_median")
-        line["efficiency"] = {"board_power_w": pw, "gflops_per_w": (value / world / pw) if pw else None,
-                              "paper": "LU 0.076 Gflops/W RX7900 + host, AC wall (P:591)"}
-
-    # ---- roofline of the dominant kernel (GEMM), timed alone on this stream --
-    if args.workload == "gemm" and rank == 0:
-        line["roofline"] = gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream)
-
-    # ---- end to end through the C ABI with HOST buffers ----------------------
     if args.workload == "gemm":
+        # ---- configs[1]: inputs resident in HBM (converted by our posit_from_f64 kernel)
+        m = n = k = 4096
+        A64, B64, C64 = SI.config2()
+        c0, c1 = col_slab(n, world, rank) if dist_on else (0, n)
+        dA = PB.posit_from_f64(torch.from_numpy(A64).to(dev))
+        dB = PB.posit_from_f64(torch.from_numpy(np.ascontiguousarray(B64[:, c0:c1])).to(dev))
+        dC0 = PB.posit_from_f64(torch.from_numpy(np.ascontiguousarray(C64[:, c0:c1])).to(dev))
+        del A64, B64, C64
+        if dist_on and rank != 0:
+            dA.zero_()                      # only rank 0 holds A; the step broadcasts it
+        dC = dC0.clone()
+        flops = 2.0 * m * n * k             # ONE problem over all ranks (strong scaling when distributed)
+
+        def step():
+            dC.copy_(dC0)
+            if dist_on:
+                gemm_colsplit(dA, dB, dC, src=0)
+            else:
+                PB.posit_gemm(dA, dB, dC)
+        ms_per_step, clocks, launches = _timed(step, args.steps, args.warmup, stream, barrier, local, dist_on, PB)
+        value = flops / (ms_per_step * 1e-3) / 1e9
+        Cfull = _gather_cols_slabs(dC, world, n) if dist_on else dC
+        if rank == 0:
+            line = {"metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
+                    "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                    "scaling": "strong" if dist_on else "weak",
+                    "vs_baseline": None, "dtype": "posit32 (int32 ALU; every mul/add correctly rounded)",
+                    "data": "synthetic (seeded numpy PCG64, BASELINE recipe)", "config": _config(args, world, dist_on),
+                    "clocks": clocks, "gpu_launches": launches,
+                    "parity": parity_vs_oracle("C2", Cfull.cpu().numpy()),
+                    "paper_context": {"gemm_gflops_rtx4090_n8000": 181.4, "gemm_gflops_agilex_n8000": 202.7,
+                                      "lu_gflops_rx7900_n8000": 13.4, "source": "PAPER.md:403,432,542"}}
+            pw = clocks.get("power_w_median")
+            line["efficiency"] = {"board_power_w": pw, "gflops_per_w": (value / world / pw) if pw else None,
+                                  "paper": "LU 0.076 Gflops/W RX7900 + host, AC wall (P:591)"}
+            # ---- roofline of the dominant kernel (this rank's GEMM), timed alone on this stream
+            line["roofline"] = gemm_roofline(PB, dA, dB, dC, dC0, m, c1 - c0, k, stream)
+        del Cfull
+        # ---- end to end through the C ABI with HOST buffers (this rank's slab)
         hA = torch.from_numpy(dA.cpu().numpy()).pin_memory()
         hB = torch.from_numpy(dB.cpu().numpy()).pin_memory()
         hC0 = dC0.cpu()
         hC = hC0.clone().pin_memory()
-        work = torch.empty(PB.posit_gemm_host_work_bytes(m, n, k), dtype=torch.uint8, device=dev)
+        work = torch.empty(PB.posit_gemm_host_work_bytes(m, c1 - c0, k), dtype=torch.uint8, device=dev)
         for _ in range(2):
             hC.copy_(hC0)
             PB.posit_gemm_host(hA, hB, hC, work)
@@ -341,32 +402,93 @@ def run_ours(args):
             hC.copy_(hC0)
             PB.posit_gemm_host(hA, hB, hC, work)
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        e2e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
+        e2e = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+        if dist_on:
             dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
         if rank == 0:
-            line["e2e"] = {"value": world * flops / float(e2e.item()) / 1e9, "unit": "Gflop/s",
-                           "h2d_bytes_per_step": 3 * m * k * 4, "d2h_bytes_per_step": m * n * 4,
-                           "api": "posit_gemm_host (pinned host A, B, C; H2D + kernel + D2H + sync per step)"}
+            line["e2e"] = {"value": flops / float(e2e.item()) / 1e9, "unit": "Gflop/s",
+                           "h2d_bytes_per_step": world * (m * k + k * (c1 - c0)) * 4 if dist_on else 3 * m * k * 4,
+                           "d2h_bytes_per_step": m * n * 4,
+                           "api": "posit_gemm_host per rank on its slab (pinned host A, B, C; "
+                                  "H2D + kernel + D2H + sync per step)"}
+            if dist_on:
+                line["e2e"]["h2d_bytes_per_step"] = world * m * k * 4 + k * n * 4 + m * n * 4
+        del dA, dB, dC, dC0, work
+        torch.cuda.empty_cache()
+        # ---- LU (configs[3]) and Cholesky (configs[2]) at this N: the metric's other two rows
+        if not args.no_factor_keys:
+            for kind, key in (("lu", "lu_c4"), ("cholesky", "chol_c3")):
+                r = factor_key(kind, args, dev, stream, barrier, local, rank, world, dist_on, PB)
+                if rank == 0:
+                    line[key] = r
+    else:
+        r = factor_key("lu" if args.workload == "lu" else "cholesky", args, dev, stream, barrier, local, rank,
+                       world, dist_on, PB)
+        if rank == 0:
+            line = {"metric": METRIC, "value": r["value"], "unit": "Gflop/s", "n_gpus": world,
+                    "steps": r["steps"], "warmup": r["warmup"], "ms_per_step": r["ms_per_step"],
+                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                    "dtype": "posit32 (int32 ALU; every mul/add correctly rounded)",
+                    "data": "synthetic (seeded numpy PCG64, BASELINE recipe)",
+                    "config": _config(args, world, dist_on), "clocks": r["clocks"],
+                    "gpu_launches": r["gpu_launches"], "parity": r["parity"]}
 
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+def _gather_cols_slabs(dC, world, n):
+    """C (m x n) from the ranks' contiguous column slabs (col_slab)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2401_14117_b200.dist import col_slab
+    m = dC.shape[0]
+    q = col_slab(n, world, 0)[1]
+    buf = torch.zeros((m, q), dtype=dC.dtype, device=dC.device)
+    buf[:, : dC.shape[1]] = dC
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    out = torch.empty((m, n), dtype=dC.dtype, device=dC.device)
+    for r in range(world):
+        c0, c1 = col_slab(n, world, r)
+        out[:, c0:c1] = parts[r][:, : c1 - c0]
+    return out
+
+
+def kernel_sass_sha(kernel_mangled: str):
+    """SHA-256 of the SASS of one kernel of the loaded library (cuobjdump), so a
+    stored ncu instruction count can be checked against the binary that runs."""
+    import hashlib
+    import re
+    import paper_2401_14117_b200 as PB
+    lib = PB.lib()._name
+    exe = "cuobjdump"
+    for cand in ("/usr/local/cuda/bin/cuobjdump",):
+        if os.path.exists(cand):
+            exe = cand
+    try:
+        txt = subprocess.run([exe, "-sass", "-fun", kernel_mangled, lib], capture_output=True, text=True,
+                             timeout=120).stdout
+    except Exception:
+        return None
+    body = [l.strip() for l in txt.split("\n") if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l)]
+    return hashlib.sha256("\n".join(body).encode()).hexdigest() if body else None
+
+
 def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):
     """Issue-bound integer roofline of the GEMM kernel, timed live with CUDA events
-    on the launching stream (copy excluded), against 148 SMs x 128 lanes x clock."""
+    on the launching stream (copy excluded), against SMs x 128 lanes x clock."""
     import torch
     peaks = _load_json(PEAKS_PATH) or {}
     prof = _load_json(PROFILE_PATH) or {}
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     times = []
     for _ in range(5):
         dC.copy_(dC0)
@@ -379,16 +501,18 @@ def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):
     t = float(np.median(times))
     macs = float(m) * n * k
     inst_per_mac = prof.get("inst_per_mac")
-    src = "ncu smsp__inst_executed.sum x 32 / MACs (profiles/gemm_kernel_profile.json)"
+    src = f"ncu smsp__inst_executed.sum x 32 / MACs (profiles/gemm_kernel_profile.json, {prof.get('tag')})"
     if inst_per_mac is None:
         inst_per_mac = prof.get("static_inst_per_mac", 54.1)
         src = "static SASS count of the inner loop (tools/sass_stats.py); no ncu capture yet"
-    peak = N_SM * LANES_PER_SM * f_max / 1e12
+    sass = kernel_sass_sha(prof["kernel_mangled"]) if prof.get("kernel_mangled") else None
+    peak = n_sm * LANES_PER_SM * f_max / 1e12
     achieved = macs * inst_per_mac / t / 1e12
     return {"bound": "alu", "unit": "Tinst/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
             "traffic": prof.get("dram_bytes_per_launch"), "kernel": prof.get("kernel", "pg::k_gemm (NN)"),
             "kernel_ms": t * 1e3, "inst_per_mac": inst_per_mac, "inst_per_mac_source": src,
-            "peak_source": f"148 SMs x 4 SMSP x 32 lanes x sm_max_mhz {f_max / 1e6:.0f} (MEASURED_PEAKS.json) "
+            "sass_sha256": sass, "inst_per_mac_stale": (None if sass is None else sass != prof.get("sass_sha256")),
+            "peak_source": f"{n_sm} SMs x 4 SMSP x 32 lanes x sm_max_mhz {f_max / 1e6:.0f} (MEASURED_PEAKS.json) "
                            "= warp-instruction issue limit; see DESIGN.md",
             "posit_tflops_kernel": 2 * macs / t / 1e12}
 
@@ -401,6 +525,10 @@ def main():
     ap.add_argument("--workload", choices=["gemm", "lu", "cholesky"], default="gemm")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the distributed (NCCL) schedules even at world size 1")
+    ap.add_argument("--no-factor-keys", action="store_true", help="skip the lu_c4 / chol_c3 keys")
+    ap.add_argument("--factor-steps", type=int, default=3, help="timed steps of the lu_c4 / chol_c3 keys")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -163,8 +163,12 @@ int posit_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, i
 
 /*
  * posit_getrf_panel -- unblocked LU with partial pivoting of the m x b panel
- * A (the panel step of posit_getrf; used by the multi-GPU driver).  Row swaps
- * are applied inside the panel only.  ipiv[j] receives row_base + p + 1
+ * A (the panel step of posit_getrf; used by the multi-GPU driver).  The same
+ * per-column operations as posit_getrf (pivot by signed compare of abs
+ * patterns, Q10; one posit division per multiplier, Q8; zero pivot -> info,
+ * Q11), i.e. LAPACK's getf2 step that MPLAPACK's Rgetrf runs on the host in
+ * the paper.  Row swaps are applied inside the
+ * panel only.  ipiv[j] receives row_base + p + 1
  * (1-based, offset by row_base); *info, if still 0, receives row_base + j + 1
  * at the first zero pivot.  work: DEVICE workspace of posit_getrf_work_bytes()
  * bytes (else -8).
@@ -174,7 +178,12 @@ int posit_getrf_panel(int64_t m, int64_t b, uint32_t* A, int64_t lda, int32_t* i
 
 /*
  * posit_laswp -- apply the row interchanges ipiv[k1..k2) in order to columns
- * [0, ncols) of A: for k = k1..k2-1, swap rows k and ipiv[k]-1-ipiv_base.
+ * [0, ncols) of A: for k = k1..k2-1, swap rows k and ipiv[k]-1-ipiv_base
+ * (LAPACK laswp, the row-interchange step of the blocked Rgetrf, P:157,
+ * P:505-516; "swap rows k and p across the full width").  Pure
+ * data movement (bit copies, no arithmetic).  ipiv is DEVICE int32 with at
+ * least k2 entries; rows k1..k2-1 and every ipiv[k]-1-ipiv_base must lie in
+ * [0, number of rows of A).  Returns -i for a bad i-th argument.
  */
 int posit_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, const int32_t* ipiv,
                 int64_t ipiv_base, void* stream);

@@ -13,6 +13,44 @@ static std::atomic<unsigned long long> g_launches{0};
 
 void pb_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int pb_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0) { (void)cudaGetLastError(); d = 0; }
+  return d;
+}
+
+// per-device caches (0 = not yet queried)
+static std::atomic<int> g_nsm[PB_MAX_DEVICES];
+static std::atomic<int> g_coop[PB_MAX_DEVICES];
+
+int pb_num_sms() {
+  const int d = pb_device() % PB_MAX_DEVICES;
+  int v = g_nsm[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, pb_device()) != cudaSuccess || v <= 0) {
+      (void)cudaGetLastError();
+      v = 148;                                   // B200 (sm_100a); only if the query itself fails
+    }
+    g_nsm[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+bool pb_coop_supported() {
+  const int d = pb_device() % PB_MAX_DEVICES;
+  int v = g_coop[d].load(std::memory_order_relaxed);
+  if (v == 0) {
+    int ok = 0;
+    if (cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, pb_device()) != cudaSuccess) {
+      (void)cudaGetLastError();
+      ok = 0;
+    }
+    v = ok ? 1 : -1;
+    g_coop[d].store(v, std::memory_order_relaxed);
+  }
+  return v > 0;
+}
+
 static int cuda_check(cudaError_t e) {
   if (e == cudaSuccess) return 0;
   strncpy(g_last_error, cudaGetErrorString(e), sizeof(g_last_error) - 1);
@@ -192,15 +230,22 @@ static int gemm_host_pipelined(char transb, int64_t m, int64_t n, int64_t k, uin
                                dC + r0 * n, n > 0 ? n : 1, q);
       if (g) rc = g;
     }
+    if (rc != 0) break;                          // never copy back rows that were not computed
     ck(cudaEventRecord(ev_done[i], q));
     ck(cudaStreamWaitEvent(ds, ev_done[i], 0));
     ck(cudaMemcpy2DAsync(C + r0 * ldc, (size_t)ldc * 4, dC + r0 * n, (size_t)n * 4, (size_t)n * 4, (size_t)mr,
                          cudaMemcpyDeviceToHost, ds));
   }
-  ck(cudaEventRecord(ev_end, ds));
-  ck(cudaStreamWaitEvent(st, ev_end, 0));
-  if (rc == 0) ck(cudaStreamSynchronize(st));
-  else cudaStreamSynchronize(ds);
+  if (rc == 0) {
+    ck(cudaEventRecord(ev_end, ds));
+    ck(cudaStreamWaitEvent(st, ev_end, 0));
+    if (rc == 0) ck(cudaStreamSynchronize(st));
+  }
+  if (rc != 0) {
+    // drain every pipeline stream before returning: no copy may still be in
+    // flight into or out of the caller's host buffers
+    for (cudaStream_t q : {cs, ks[0], ks[1], ds}) (void)cudaStreamSynchronize(q);
+  }
   return rc;
 }
 
@@ -212,6 +257,13 @@ int posit_gemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, u
   if (m < 0) return -3;
   if (n < 0) return -4;
   if (k < 0) return -5;
+  if (alpha != POSIT_ONE && alpha != POSIT_MONE) return -6;
+  if (lda < ((transa == 'N' ? k : m) > 1 ? (transa == 'N' ? k : m) : 1)) return -8;
+  if (ldb < ((transb == 'N' ? n : k) > 1 ? (transb == 'N' ? n : k) : 1)) return -10;
+  if (beta != 0u && beta != POSIT_ONE) return -11;
+  if (ldc < (n > 1 ? n : 1)) return -13;
+  if (m == 0 || n == 0) return 0;
+  if ((k > 0 && (A == nullptr || B == nullptr)) || C == nullptr) return -7;
   if (work_bytes < posit_gemm_host_work_bytes(m, n, k) || dwork == nullptr) return -15;
   const int64_t brow = transb == 'N' ? k : n, bcol = transb == 'N' ? n : k;
   const int64_t arow = transa == 'N' ? m : k, acol = transa == 'N' ? k : m;
@@ -332,7 +384,7 @@ static int64_t tail_w() {                       // POSIT_TAIL_W: width of the fu
   }();
   return v;
 }
-static int64_t tail_m() { return 148 * 40; }      // rows: 40 per CTA x 1024 columns fit 160 KB
+static int64_t tail_m() { return (int64_t)pb_num_sms() * 40; }   // rows: 40 per CTA x 1024 columns fit 160 KB
 
 static int64_t wide_leaf_cols() {
   static const int64_t v = [] {

@@ -478,14 +478,13 @@ int launch_cfg(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, boo
   const size_t smem = sizeof(typename C::Smem);
   auto kern = transb ? (syrk ? pg::k_gemm<C, true, true> : pg::k_gemm<C, true, false>)
                      : (syrk ? pg::k_gemm<C, false, true> : pg::k_gemm<C, false, false>);
-  static const bool attrs = [smem] {           // thread-safe one-time init, all four instantiations
+  static PbOncePerDevice attrs;                // one-time init per device, all four instantiations
+  pb_once_per_device(attrs, [smem] {
     cudaFuncSetAttribute(pg::k_gemm<C, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(pg::k_gemm<C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(pg::k_gemm<C, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(pg::k_gemm<C, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return true;
-  }();
-  (void)attrs;
+  });
   pb_count_launch();
   if (pdl) {
     // programmatic dependent launch: this grid may start while the previous
@@ -517,15 +516,15 @@ int variant() {
 }
 
 // Modelled time of a launch with config C: the busiest SM runs ceil(tiles /
-// 148) CTAs of NTHR x 16 accumulators each; an SM with 512 resident threads
+// SMs) CTAs of NTHR x 16 accumulators each; an SM with 512 resident threads
 // issues at the full rate, one with only 256 (a lone small CTA) at ~2/3 of it
 // (measured: tools/tune_gemm.py, tall-narrow and short-wide trailing shapes).
 template <class C>
-double model_time(int64_t m, int64_t n, bool syrk) {
+double model_time(int64_t m, int64_t n, bool syrk, int64_t nsm) {
   const int64_t rb = (m + C::BM - 1) / C::BM, cb = (n + C::BN - 1) / C::BN;
   int64_t tiles = rb * cb;
   if (syrk) tiles = tiles / 2 + rb;                       // lower-triangle tiles (approx.)
-  const int64_t per_sm = (tiles + 147) / 148;
+  const int64_t per_sm = (tiles + nsm - 1) / nsm;
   const int64_t resident = (per_sm < C::MINB ? per_sm : C::MINB) * C::NTHR;
   const double rate = (resident >= 512 ? 1.0 : 0.66) * C::EFF;
   return (double)per_sm * C::BM * C::BN / rate;
@@ -573,9 +572,10 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st,
       return vb;
     };
     const int base = syrk ? 12 : 11;
-    v = pick(base, base == 12 ? model_time<G2>(P.m, P.n, syrk) : model_time<G1>(P.m, P.n, syrk),
-             {{base == 12 ? 11 : 12, base == 12 ? model_time<G1>(P.m, P.n, syrk) : model_time<G2>(P.m, P.n, syrk)},
-              {13, model_time<G3>(P.m, P.n, syrk)}, {14, model_time<G4>(P.m, P.n, syrk)}});
+    const int64_t ns = pb_num_sms();
+    v = pick(base, base == 12 ? model_time<G2>(P.m, P.n, syrk, ns) : model_time<G1>(P.m, P.n, syrk, ns),
+             {{base == 12 ? 11 : 12, base == 12 ? model_time<G1>(P.m, P.n, syrk, ns) : model_time<G2>(P.m, P.n, syrk, ns)},
+              {13, model_time<G3>(P.m, P.n, syrk, ns)}, {14, model_time<G4>(P.m, P.n, syrk, ns)}});
   }
   switch (v) {
     case 12: return launch_cfg<G2>(P, transb, syrk, st, pdl);

@@ -17,7 +17,7 @@
 //    posit fraction width f_s(E) = 27 - t(E), t(E) = (E ^ (E >> 31)) >> 2,
 //    directly in the decoded domain (valid while f_s >= 1, |E| <= 107);
 //  * rounding is RNE via two carry-chained adds (no masks, no branches);
-//  * a k-tile that contains a zero, NaR or |scale| > 53 operand is run by the
+//  * a k-tile that contains a zero, NaR or |scale| > 37 (E_STAGE_MAX) operand is run by the
 //    generic per-operation path (uniform branch for the whole CTA); an
 //    accumulator whose sum leaves |E| <= 107 marks the thread, which then
 //    recomputes its outputs with the generic path.  An exact cancellation
@@ -99,7 +99,7 @@ struct Params {
 // ---- staging decode --------------------------------------------------------
 // A side: significand hidden bit at 31.  B side: hidden bit at 30.
 // Staged element = {M, E, sigma (+1 / -1 as int), 0}.  Returns "special"
-// (zero, NaR, |E| > 53) through `special`.
+// (zero, NaR, |E| > E_STAGE_MAX = 37) through `special`.
 template <int HID, uint32_t WM = 16u, uint32_t SOFF = 0u>
 __device__ __forceinline__ uint4 stage_decode(uint32_t x, uint32_t flip, uint32_t& special, uint32_t wbase = 0u) {
   const uint32_t s = (x >> 31) ^ flip;

@@ -38,3 +38,19 @@ int pb_gemm_guarded(const pg::Params& P, bool transb, bool syrk, const int32_t* 
 
 // number of kernels this library has launched (posit_kernel_launches)
 void pb_count_launch();
+
+// Per-device facts and one-time init.  Kernel attributes (dynamic shared
+// memory limits) and the SM count belong to a device, so everything cached is
+// keyed by the current device (capi.cu), never by a process-wide static.
+#include <mutex>
+#include <utility>
+constexpr int PB_MAX_DEVICES = 64;
+int pb_device();             // current CUDA device (0 if the query fails)
+int pb_num_sms();            // multiprocessor count of the current device (cached per device)
+bool pb_coop_supported();    // cooperative launch support of the current device (cached per device)
+struct PbOncePerDevice { std::once_flag flag[PB_MAX_DEVICES]; };
+template <class F>
+inline void pb_once_per_device(PbOncePerDevice& once, F&& fn) {
+  const int d = pb_device();
+  std::call_once(once.flag[d < PB_MAX_DEVICES ? d : PB_MAX_DEVICES - 1], std::forward<F>(fn));
+}

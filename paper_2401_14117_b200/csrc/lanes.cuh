@@ -123,13 +123,15 @@ __device__ __forceinline__ void lv_fms_t(LaneVal& c, uint32_t ap, bool afast, co
 
 inline unsigned grid_for(int64_t count, int threads) {
   int64_t g = (count + threads - 1) / threads;
-  if (g > 148 * 64) g = 148 * 64;
+  const int64_t cap = (int64_t)pb_num_sms() * 64;
+  if (g > cap) g = cap;
   return (unsigned)(g < 1 ? 1 : g);
 }
 
 inline unsigned rows_grid(int64_t rows, int threads) {
   int64_t g = (rows + threads - 1) / threads;
-  if (g > 148 * 4) g = 148 * 4;
+  const int64_t cap = (int64_t)pb_num_sms() * 4;
+  if (g > cap) g = cap;
   return (unsigned)(g < 1 ? 1 : g);
 }
 

@@ -384,22 +384,17 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
                       LeafWs* ws, bool allow_coop, cudaStream_t st) {
   if (cudaMemsetAsync(ws, 0, LEAF_WS_ZERO, st) != cudaSuccess) return POSIT_ECUDA;
   // one cooperative launch when the rows fit the CTAs' shared memory
-  struct CoopCfg { int coop; int nsm; };
-  static const CoopCfg cfg = [] {
-    CoopCfg c{1, 148};
+  static const int coop_env = [] {
     const char* e = getenv("POSIT_LEAF_COOP");
-    c.coop = e ? atoi(e) : 1;
-    int dev = 0, ok = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
-    if (!ok) c.coop = 0;
+    return e ? atoi(e) : 1;
+  }();
+  static PbOncePerDevice attrs;
+  pb_once_per_device(attrs, [] {
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(k_leaf_coop1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(k_leaf_coop1<TAIL_WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    return c;
-  }();
-  const int coop = cfg.coop, nsm = cfg.nsm;
+  });
+  const int coop = pb_coop_supported() ? coop_env : 0, nsm = pb_num_sms();
   // on the caller's stream: one CTA of 256 threads per SM; on a side stream
   // (lookahead, sharing the SMs with the trailing GEMM): a few CTAs of 1024
   static const int force = [] {                 // POSIT_LEAF_CTAS = 16 / 148: force one configuration (tests, sweeps)
@@ -465,9 +460,7 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
 int pb_getrf_tail(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t row_base,
                   void* ws, cudaStream_t st) {
   if (m <= 0 || w <= 0) return 0;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = pb_num_sms();
   const int64_t rpc = (m + nsm - 1) / nsm;
   if (w > TAIL_WMAX || (size_t)rpc * (size_t)w * sizeof(uint32_t) > 160 * 1024) return POSIT_ENOTSUP;
   return getrf_leaf(m, w, A, lda, ipiv, info, row_base, static_cast<LeafWs*>(ws), true, st);

@@ -129,12 +129,11 @@ int pb_solve(bool chol, int64_t n, const uint32_t* A, int64_t lda, const int32_t
   if (n <= 0) return 0;
   const size_t smem = (size_t)n * sizeof(uint32_t);
   if (smem > 200 * 1024) return POSIT_ENOTSUP;
-  static const bool attr = [] {
+  static PbOncePerDevice attrs;
+  pb_once_per_device(attrs, [] {
     cudaFuncSetAttribute(k_getrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_potrs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    return true;
-  }();
-  (void)attr;
+  });
   pb_count_launch();
   if (chol) k_potrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, b);
   else k_getrs<<<1, SOLVE_THREADS, smem, st>>>(n, A, lda, ipiv, b);

@@ -135,10 +135,10 @@ int pb_laswp(int64_t ncols, uint32_t* A, int64_t lda, int64_t k1, int64_t k2, co
              cudaStream_t st) {
   if (ncols <= 0 || k2 <= k1) return 0;
   constexpr size_t smem = 2 * SWP_MAX * SWP_COLS * sizeof(uint32_t);
-  static const bool attr = [] {
-    return cudaFuncSetAttribute(k_laswp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-  }();
-  (void)attr;
+  static PbOncePerDevice attrs;
+  pb_once_per_device(attrs, [] {
+    cudaFuncSetAttribute(k_laswp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
   pb_count_launch();
   k_laswp<<<(unsigned)((ncols + SWP_COLS - 1) / SWP_COLS), 256, smem, st>>>(A, lda, ncols, k1, k2, ipiv, ipiv_base);
   return last_launch();

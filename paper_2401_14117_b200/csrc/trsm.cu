@@ -510,7 +510,7 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
     const int v = e == nullptr ? -1 : atoi(e);
     return v == 0 || v == 4 || v == 8 ? v : -1;
   }();
-  const int use_col = col_env >= 0 ? col_env : (n > 148 * TB ? 4 : 0);
+  const int use_col = col_env >= 0 ? col_env : (n > (int64_t)pb_num_sms() * TB ? 4 : 0);
   static const int blk_env = [] {                 // warp-per-column CTA width: 8 (default) or 32 columns
     const char* e = getenv("POSIT_LLNU_BLK");
     return e ? atoi(e) : 8;
@@ -548,6 +548,10 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
       const char* e = getenv("POSIT_RLTN");
       int w = 16, r = 16;
       if (e) sscanf(e, "%d,%d", &w, &r);
+      return w * 100 + r;
+    }();
+    static PbOncePerDevice attrs;
+    pb_once_per_device(attrs, [] {
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -556,8 +560,7 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
                            (int)sizeof(FrSmem<8, 16>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<8, 32>));
-      return w * 100 + r;
-    }();
+    });
     pb_count_launch();
 #define PB_RLTN(W_, R_)                                                                                              \
   k_trsm_rltn_fused<W_, R_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(L, ldl, B, ldb, m, \

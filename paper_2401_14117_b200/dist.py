@@ -96,6 +96,13 @@ class BlockCyclic1D:
         return out
 
 
+def _collective(P: int, group) -> bool:
+    """Broadcast whenever a process group exists -- also at P = 1 (bench.py
+    --force-dist), so the NCCL / side-stream / record_stream path of the
+    schedule runs on a one-GPU lease exactly as it does at P > 1."""
+    return P > 1 or group is not None or (dist.is_available() and dist.is_initialized())
+
+
 class CudaOps:
     """The product arithmetic: libposit_b200.so through the package binding."""
 
@@ -138,7 +145,7 @@ def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, i
     if not cuda:
         steps = getrf_dist_steps(A_local, desc, ipiv, info, ops)
         for s, buf in steps:
-            if P > 1:
+            if _collective(P, group):
                 dist.broadcast(buf, src=desc.owner(s), group=group)
         return
     main = torch.cuda.current_stream()
@@ -163,7 +170,7 @@ def getrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, ipiv: torch.Tensor, i
     steps = getrf_dist_steps(A_local, desc, ipiv, info, ops, panel_ctx=_OnSide, on_use=on_use)
     for s, buf in steps:
         buf.record_stream(side)              # allocated on the main stream, used on the side stream too
-        if P > 1:
+        if _collective(P, group):
             with torch.cuda.stream(side):
                 side.wait_stream(main)
                 pending[s] = dist.broadcast(buf, src=desc.owner(s), group=group, async_op=True)
@@ -319,7 +326,7 @@ def potrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, info: torch.Tensor, o
     P = desc.nprocs
     if not cuda:
         for s, buf in potrf_dist_steps(A_local, desc, info, ops):
-            if P > 1:
+            if _collective(P, group):
                 dist.broadcast(buf, src=desc.owner(s), group=group)
         return
     main = torch.cuda.current_stream()
@@ -343,7 +350,7 @@ def potrf_dist(A_local: torch.Tensor, desc: BlockCyclic1D, info: torch.Tensor, o
 
     for s, buf in potrf_dist_steps(A_local, desc, info, ops, panel_ctx=_OnSide, on_use=on_use):
         buf.record_stream(side)
-        if P > 1:
+        if _collective(P, group):
             with torch.cuda.stream(side):
                 side.wait_stream(main)
                 pending[s] = dist.broadcast(buf, src=desc.owner(s), group=group, async_op=True)
@@ -413,3 +420,31 @@ def potrf_dist_steps(A_local, desc: BlockCyclic1D, info, ops, panel_ctx=None, on
                 if j != s + 1:
                     update_block(s, panel, j)
             buf = nxt
+
+
+# ------------------------------------------------------------------ GEMM ------
+# SURVEY 8(e) "GEMM (C2): split C by column blocks.  Each rank needs A
+# (broadcast) and its B slab.  No split-K (forbidden by c4) and no reduction."
+# One m x n x k problem over P ranks (strong scaling): rank r owns the
+# contiguous column slab [c0_r, c1_r) of B and C; A lives on rank `src` and is
+# sent to every rank with ONE broadcast per call; then each rank runs
+# C_r <- C_r - A . B_r on its own slab.  Every output element's chain is the
+# single-GPU one (DESIGN.md Q6), so the gathered C is bit-identical for every P.
+
+def col_slab(n: int, nprocs: int, rank: int) -> tuple[int, int]:
+    """[c0, c1) of rank's column slab: contiguous, balanced, multiples of 4
+    columns (16-byte rows for the kernels' quad loads) except the last."""
+    q = (n + 4 * nprocs - 1) // (4 * nprocs) * 4
+    c0 = min(n, rank * q)
+    return c0, min(n, c0 + q)
+
+
+def gemm_colsplit(A: torch.Tensor, B_local: torch.Tensor, C_local: torch.Tensor, src: int = 0,
+                  ops=None, group=None) -> None:
+    """C_local <- C_local - A . B_local on this rank's column slab, after ONE
+    broadcast of A (m x k, allocated on every rank; its contents matter on
+    `src` only) from rank `src`."""
+    ops = CudaOps() if ops is None else ops
+    if dist.is_available() and dist.is_initialized():
+        dist.broadcast(A, src=src, group=group)
+    ops.gemm_minus(A, B_local, C_local)

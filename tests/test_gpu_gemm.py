@@ -64,10 +64,12 @@ def test_gemm_alpha_beta(cuda_ok, alpha, beta):
     assert mismatch(_gpu_gemm(A, B, C, alpha=alpha, beta=beta), O.gemm(A, B, C, alpha=alpha, beta=beta)) == 0
 
 
-def test_gemm_special_values_and_cancellation(cuda_ok):
-    # zeros, NaR, huge/tiny magnitudes (slow k-slabs), exact cancellations (integers)
+@pytest.mark.parametrize("m,n,k", [(70, 140, 80), (300, 520, 80)])
+def test_gemm_special_values_and_cancellation(cuda_ok, m, n, k):
+    # zeros, NaR, huge/tiny magnitudes (slow k-slabs), exact cancellations (integers);
+    # 300 x 520 is above the one-thread-per-output cutoff, so the tiled k_gemm's
+    # generic slab and thread-recompute paths run (70 x 140 takes k_gemm_tiny)
     rng = np.random.default_rng(3)
-    m, n, k = 70, 140, 80
     A = rng.integers(-3, 4, (m, k)).astype(np.float64)
     B = rng.integers(-3, 4, (k, n)).astype(np.float64)
     C = rng.integers(-5, 6, (m, n)).astype(np.float64)
@@ -133,14 +135,15 @@ def test_gemm_bad_arguments(cuda_ok):
         PB.posit_gemm(A, A, A, beta=O.from_f64(0.5))
 
 
+@pytest.mark.parametrize("m,n", [(70, 130), (300, 520)])
 @pytest.mark.parametrize("ea,ec", [(36, 88), (38, 92), (-36, -100), (-38, 40), (30, 100)])
-def test_gemm_fast_path_range_boundaries(cuda_ok, ea, ec):
+def test_gemm_fast_path_range_boundaries(cuda_ok, ea, ec, m, n):
     # operand scales straddling the staging limit (|E| <= 37 -> fast slab) and
     # accumulator scales straddling the per-slab limit (|E| <= 91), plus growth
     # within a slab: the fast path, the generic slab and the thread recompute
     # must all give the oracle's bits
     rng = np.random.default_rng(abs(ea) * 1000 + abs(ec))
-    m, n, k = 70, 130, 48
+    k = 48
     A = np.ldexp(rng.uniform(1.0, 2.0, (m, k)) * rng.choice([-1.0, 1.0], (m, k)), ea + rng.integers(-2, 3, (m, k)))
     B = np.ldexp(rng.uniform(1.0, 2.0, (k, n)) * rng.choice([-1.0, 1.0], (k, n)), ea + rng.integers(-2, 3, (k, n)))
     C = np.ldexp(rng.standard_normal((m, n)), ec + rng.integers(-3, 4, (m, n)))
