@@ -9,6 +9,9 @@ never does, and shares no code with it.
   textbook unblocked LU / Cholesky / GEMM in the order contract), OpenMP over
   independent output elements.
 * ``checker.py`` -- exact ``Fraction`` checker that pins the C oracle.
+* ``checker_wide.c`` / ``checker_wide.py`` -- checker.py's definitions with
+  exact 768-bit integer comparisons (pinned to checker.py), fast enough for
+  S:443's 1e7 random pairs per operation (tests/test_oracle_wide.py).
 * ``make_golden.py`` -- writes ``tests/golden/`` digests by calling only the
   oracle and the seeded input generators.
 

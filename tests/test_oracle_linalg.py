@@ -290,7 +290,7 @@ def test_getrs_dyadic_exact_with_pivots():
     LU, ipiv, info = O.getrf(P(A))
     assert info == 0
     got = F(O.getrs(LU, ipiv, P(A @ x)))
-    np.testing.assert_allclose(got, x, rtol=0, atol=1e-6)
+    assert np.array_equal(got, x), (got, x)         # every intermediate exact: x recovered bit for bit
 
 
 def _checker_back_desc(U, y):
