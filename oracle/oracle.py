@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
             L.or_trsm_rltn.restype = i32
             L.or_getrf.argtypes = [i64, i64, vp, i64, vp, vp]
             L.or_getrf.restype = i32
+            L.or_getrf_steps.argtypes = [i64, i64, vp, i64, vp, vp, i64, i64]
+            L.or_getrf_steps.restype = i32
             L.or_potrf_lower.argtypes = [i64, vp, i64, vp]
             L.or_potrf_lower.restype = i32
             L.or_getrs.argtypes = [i64, vp, i64, vp, vp]
@@ -196,6 +198,16 @@ def getrf(A) -> tuple[np.ndarray, np.ndarray, int]:
     info = np.zeros(1, np.int32)
     lib().or_getrf(m, n, _ptr(A), n, _ptr(ipiv), _ptr(info))
     return A, ipiv, int(info[0])
+
+
+def getrf_steps(A, ipiv, info, k0: int, k1: int) -> None:
+    """Steps k0 <= k < k1 of the textbook LU in place on A (uint32, C-contiguous),
+    ipiv (int32) and info (int32 array of 1): resumable form of getrf."""
+    assert A.flags.c_contiguous and A.dtype == np.uint32 and ipiv.dtype == np.int32 and info.dtype == np.int32
+    m, n = A.shape
+    rc = lib().or_getrf_steps(m, n, _ptr(A), n, _ptr(ipiv), _ptr(info), k0, k1)
+    if rc != 0:
+        raise ValueError(f"or_getrf_steps returned {rc}")
 
 
 def potrf_lower(A) -> tuple[np.ndarray, int]:

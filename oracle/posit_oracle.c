@@ -442,12 +442,16 @@ static inline int32_t pabs_key(uint32_t a) {    /* abs by negation; compared as 
  *   ipiv_k = p+1; if a_pk != 0: swap rows k,p (full width), a_ik <- a_ik (/) a_kk
  *   else info <- info or k+1
  *   a_ij <- a_ij (-) a_ik (x) a_kj for i > k, j > k                      */
-int or_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info) {
+/* or_getrf_steps runs this loop's steps k in [k0, k1) only, so that a long run
+ * (configs[3], n = 16384) can be checkpointed between steps (A, ipiv, info)
+ * and resumed; or_getrf is all steps from a zeroed info.  Same arithmetic. */
+int or_getrf_steps(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info, int64_t k0,
+                   int64_t k1) {
     if (m < 0) return -1;
     if (n < 0) return -2;
-    *info = 0;
     const int64_t kmax = m < n ? m : n;
-    for (int64_t k = 0; k < kmax; k++) {
+    if (k1 > kmax) k1 = kmax;
+    for (int64_t k = k0; k < k1; k++) {
         int64_t p = k;
         int32_t best = pabs_key(A[k * lda + k]);
         for (int64_t i = k + 1; i < m; i++) {
@@ -473,6 +477,13 @@ int or_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int3
         }
     }
     return 0;
+}
+
+int or_getrf(int64_t m, int64_t n, uint32_t* A, int64_t lda, int32_t* ipiv, int32_t* info) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    *info = 0;
+    return or_getrf_steps(m, n, A, lda, ipiv, info, 0, m < n ? m : n);
 }
 
 /* Textbook right-looking Cholesky, lower, SURVEY 8(c) c4 / Q9:

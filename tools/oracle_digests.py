@@ -81,6 +81,43 @@ def inputs(cfg: str):
     return {"A": O.from_f64_array(SI.config5(C5_NAMES[cfg]))}
 
 
+def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budget_s: float, chunk: int = 64):
+    """The textbook LU in chunks of `chunk` steps (or_getrf_steps: the same loop),
+    checkpointed to ckpt_dir (A, ipiv, info, next step) when the time budget
+    would run out; resumes from a checkpoint of the same input.  -> (LU, ipiv,
+    info) or None if stopped at a checkpoint."""
+    t0 = t_call = time.time()
+    os.makedirs(ckpt_dir, exist_ok=True)
+    base = os.path.join(ckpt_dir, f"{cfg}_{in_sha[:16]}")
+    if os.path.exists(base + ".json"):
+        st = json.load(open(base + ".json"))
+        A = np.load(base + "_A.npy")
+        ipiv = np.load(base + "_ipiv.npy")
+        info = np.array([st["info"]], np.int32)
+        k = st["k"]
+        t0 -= st.get("elapsed", 0.0)                 # report the whole run's oracle time
+        print(f"{cfg}: resuming at step {k} of {A.shape[0]} (checkpoint)", flush=True)
+    else:
+        A, ipiv, info, k = A0.copy(), np.zeros(min(A0.shape), np.int32), np.zeros(1, np.int32), 0
+    kmax = min(A.shape)
+    last = 0.0
+    while k < kmax:
+        if budget_s > 0 and time.time() - t_call + 1.3 * last + 30 > budget_s:
+            np.save(base + "_A.npy", A)
+            np.save(base + "_ipiv.npy", ipiv)
+            json.dump({"k": k, "info": int(info[0]), "elapsed": time.time() - t0}, open(base + ".json", "w"))
+            print(f"{cfg}: checkpoint at step {k} of {kmax} after {time.time() - t0:.0f} s", flush=True)
+            return None
+        tc = time.time()
+        O.getrf_steps(A, ipiv, info, k, min(kmax, k + chunk))
+        last = time.time() - tc
+        k = min(kmax, k + chunk)
+    for f in (base + ".json", base + "_A.npy", base + "_ipiv.npy"):
+        if os.path.exists(f):
+            os.remove(f)
+    return A, ipiv, int(info[0]), time.time() - t0
+
+
 def run(cfg: str, X: dict):
     """-> (output matrix, ipiv or None, info or None, op description)."""
     if cfg == "C2":
@@ -92,12 +129,17 @@ def run(cfg: str, X: dict):
     return LU, ipiv, info, "or_getrf (unblocked right-looking kij, partial pivoting)"
 
 
+T_START = time.time()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default=",".join(ALL))
     ap.add_argument("--out-dir", default=OUT_DIR)
     ap.add_argument("--cache", default=os.path.join(ROOT, "oracle_cache"))
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--ckpt-dir", default=None, help="LU configs: checkpoint / resume directory")
+    ap.add_argument("--time-budget", type=float, default=0.0, help="seconds; checkpoint and stop before it runs out")
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)
     os.makedirs(args.cache, exist_ok=True)
@@ -114,8 +156,17 @@ def main() -> None:
                 continue
         print(f"{cfg}: running oracle on {O.num_threads()} threads ...", flush=True)
         t0 = time.time()
-        M, ipiv, info, what = run(cfg, X)
-        dt = time.time() - t0
+        if args.ckpt_dir and cfg not in ("C2", "C3"):
+            left = args.time_budget - (time.time() - T_START) if args.time_budget > 0 else 0.0
+            r = run_lu_resumable(cfg, X["A"], in_sha, args.ckpt_dir, left)
+            if r is None:
+                sys.exit(2)
+            M, ipiv, info, dt_total = r
+            what = "or_getrf (unblocked right-looking kij, partial pivoting; run as or_getrf_steps chunks)"
+        else:
+            M, ipiv, info, what = run(cfg, X)
+            dt_total = time.time() - t0
+        dt = dt_total
         parts = [M] + ([ipiv] if ipiv is not None else []) + ([np.array([info], np.int32)] if info is not None else [])
         rec = {
             "config": cfg,
