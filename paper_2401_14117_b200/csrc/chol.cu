@@ -75,6 +75,180 @@ __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, i
   if (in) A[i * lda + j] = lv_pattern(v);
 }
 
+// ---- the whole <= 256 x 256 diagonal block in ONE launch: a thread-block cluster --
+// Textbook right-looking loop (reading Q9) over all b columns, the lower
+// triangle distributed over the PC_NC CTAs of one cluster (distributed shared
+// memory; cluster barriers ~0.2 us instead of kernel launches or grid syncs):
+//   CTA c, warp w, lane l owns row i = l PC_NC + c, columns j = w + 32 q (q < 8),
+//   every element decoded in a register for the whole loop.
+// Step k: warp k % 32 owns column k.  Its lane k / 32 also keeps a redundant
+// copy of the diagonal chain d_k (every CTA keeps all of them: d_j <- d_j (-)
+// l_jk (x) l_jk, the same operations in the same order as the element a_jj,
+// hence the same bits), so every CTA takes l_kk = sqrt(d_k) itself and no
+// extra barrier is needed for it.  The warp divides its column-k elements by
+// l_kk (one posit division each) and pushes them into the column buffer of
+// every CTA of the cluster; one split cluster barrier per column publishes the
+// column, then every thread applies a_ij <- a_ij (-) l_ik (x) l_jk to its own
+// elements (ascending k per element: Q6).  A non-positive d_k stops every CTA
+// at the same step (info = row_base + k + 1, all steps < k applied, as the
+// oracle's loop).
+constexpr int PC_NC = 8;                       // CTAs per cluster (portable size)
+constexpr int PC_Q = 8;                        // column slots per thread
+constexpr int PC_B = 32 * PC_NC;               // 256: largest block
+
+struct PcSmem {
+  uint32_t colp[2][PC_B];                      // column k: patterns l_jk (rows j > k)
+  uint4 cola[2][PC_B];                         // A-format decode {M, E, sigma, fast}
+  uint4 colb[2][PC_B];                         // B-format decode {M, E, sg, fast}
+  int fail;
+  uint4 tp[pg::TSIZE], tx[pg::TSIZE];          // the MAC's per-scale constant tables
+};
+
+// A LaneVal in three registers (the kernel keeps nine per thread under the
+// 64-register cap of 1024-thread CTAs): decoded {M, E, sg}, or the pattern in
+// M with E = PC_PAT when the value is outside the fast range.
+constexpr int32_t PC_PAT = 0x40000000;
+struct PcVal { uint32_t M; int32_t E; int32_t sg; };
+
+__device__ __forceinline__ PcVal pc_of(const LaneVal& v) {
+  return v.dec ? PcVal{v.a.M, v.a.E, v.a.sg} : PcVal{v.pat, PC_PAT, 1};
+}
+__device__ __forceinline__ LaneVal pc_lane(const PcVal& x) {
+  LaneVal v;
+  v.dec = x.E != PC_PAT;
+  v.a = pg::Acc{x.M, x.E, x.sg};
+  v.pat = x.M;
+  return v;
+}
+
+__device__ __forceinline__ void pc_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void pc_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+__global__ void __cluster_dims__(PC_NC, 1, 1) __launch_bounds__(1024, 1)
+    k_potf2_cluster(uint32_t* A, int64_t lda, int b, int32_t* info, int64_t row_base) {
+  namespace cg = cooperative_groups;
+  __shared__ PcSmem S;
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int i = l * PC_NC + c;                                  // my row
+  const bool stop0 = *info != 0;                                // an earlier block failed: every CTA returns
+  if (stop0) return;
+  pg::fill_tables(S.tp, S.tx, threadIdx.x, 1024);
+  pg::MacConst K;
+  K.one = 1u; K.sixteen = 16u;
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
+  if (threadIdx.x == 0) S.fail = 0;
+  PcVal v[PC_Q];
+#pragma unroll
+  for (int q = 0; q < PC_Q; q++) {
+    const int j = w + 32 * q;
+    LaneVal t;
+    lv_load(t, (i < b && j <= i) ? A[(int64_t)i * lda + j] : 0u);
+    v[q] = pc_of(t);
+  }
+  PcVal dd;                                                     // redundant diagonal d_j, j = w + 32 l (l < 8)
+  const int jd = w + 32 * l;
+  {
+    LaneVal t;
+    lv_load(t, (l < PC_Q && jd < b) ? A[(int64_t)jd * lda + jd] : 0u);
+    dd = pc_of(t);
+  }
+  __syncthreads();
+  cl.sync();                                                    // every CTA running before any remote store
+  bool failed = false;
+  for (int k = 0; k < b; k++) {
+    const int qk = k & 1, qp = qk ^ 1;
+    if (k > 0) {
+      pc_wait();                                                // column k - 1 published everywhere
+      if (S.fail) { failed = true; break; }                     // same step in every CTA: barriers stay balanced
+      // this step's critical chain first: my diagonal copy and my column-k element
+      if (l < PC_Q && jd >= k && jd < b) {
+        const uint4 ad = S.cola[qp][jd], bd = S.colb[qp][jd];
+        LaneVal d = pc_lane(dd);
+        lv_fms_t(d, S.colp[qp][jd], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, S.colp[qp][jd], K);
+        dd = pc_of(d);
+      }
+    }
+    if (w == (k & 31)) {                                        // my warp owns column k
+      const int qc = k >> 5;                                    // its slot (selected, not indexed: no local memory)
+      PcVal xs = v[0];
+#pragma unroll
+      for (int q = 1; q < PC_Q; q++)
+        if (q == qc) xs = v[q];
+      LaneVal x = pc_lane(xs);
+      if (k > 0 && i < b && i >= k) {                           // step k - 1's update of my column-k element
+        const uint4 ad = S.cola[qp][i], bd = S.colb[qp][k];
+        lv_fms_t(x, S.colp[qp][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, S.colp[qp][k], K);
+      }
+      // l_kk = sqrt(d_k) in lane k / 32, broadcast to the warp
+      uint32_t dk = 0u;
+      if (l == qc) dk = lv_pattern(pc_lane(dd));
+      dk = __shfl_sync(0xFFFFFFFFu, dk, qc);
+      if ((int32_t)dk <= 0) {                                   // zero, negative or NaR pivot: stop
+        if (l == 0) {
+          S.fail = 1;
+          if (c == 0) *info = (int32_t)(row_base + k + 1);
+        }
+      } else {
+        const uint32_t lkk = p32::sqrt(dk);
+        if (i == k) lv_load(x, lkk);
+        if (i > k && i < b) {
+          pg::Acc dv;
+          const bool dok = pg::acc_decode(lkk, dv) && dv.E <= 37 && dv.E >= -37;
+          bool done = false;
+          if (dok && x.dec) {
+            done = pg::acc_div(x.a, dv.M, dv.E, dv.sg, __drcp_rn((double)dv.M) * 4294967296.0, K);
+            if (done && !(x.a.E <= 75 && x.a.E >= -75) && x.a.E > pg::E_ZERO_LIMIT) {
+              x.pat = pg::acc_encode(x.a);
+              x.dec = false;
+            }
+          }
+          if (!done) lv_load(x, div(lv_pattern(x), lkk));
+          const uint32_t xp = lv_pattern(x);
+          uint4 adx;
+          const uint4 av = fast_a(xp, adx) ? make_uint4(adx.x, adx.y, adx.z, 1u) : make_uint4(0u, 0u, 0u, 0u);
+          const uint4 bv = lv_operand(x) ? make_uint4(x.a.M, (uint32_t)x.a.E, (uint32_t)x.a.sg, 1u)
+                                         : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int r = 0; r < PC_NC; r++) {                     // push l_ik into every CTA's column buffer
+            *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
+            *cl.map_shared_rank(&S.cola[qk][i], r) = av;
+            *cl.map_shared_rank(&S.colb[qk][i], r) = bv;
+          }
+        }
+      }
+      xs = pc_of(x);
+#pragma unroll
+      for (int q = 0; q < PC_Q; q++)
+        if (q == qc) v[q] = xs;
+    }
+    // the rest of step k - 1's updates on my elements (columns j > k)
+    if (k > 0) {
+#pragma unroll
+      for (int q = 0; q < PC_Q; q++) {
+        const int j = w + 32 * q;
+        if (j > k && j <= i && i < b) {
+          const uint4 ad = S.cola[qp][i], bd = S.colb[qp][j];
+          LaneVal t = pc_lane(v[q]);
+          lv_fms_t(t, S.colp[qp][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u,
+                   S.colp[qp][j], K);
+          v[q] = pc_of(t);
+        }
+      }
+    }
+    pc_arrive();                                                // my pushes for column k (release)
+  }
+  if (!failed) pc_wait();                                       // the last arrive (a failure already waited)
+#pragma unroll
+  for (int q = 0; q < PC_Q; q++) {
+    const int j = w + 32 * q;
+    if (i < b && j <= i) A[(int64_t)i * lda + j] = lv_pattern(pc_lane(v[q]));
+  }
+  cl.sync();                                                    // no CTA exits while others may still read it
+}
+
 }  // namespace pl
 
 using namespace pl;
@@ -150,17 +324,24 @@ __global__ void __launch_bounds__(256) k_syrk_tiny(int64_t n, int64_t k, const u
   C[i * ldc + j] = lv_pattern(c);
 }
 
-// Diagonal-block Cholesky: right-looking by 32-wide block columns (leaf of
-// <= 32 in one CTA, the rows below by the fused TRSM, the trailing lower
-// triangle by the one-thread-per-element SYRK), or (POSIT_POTF2=0) the
-// recursive potrf2 traversal.  Every stage is a no-op once *info != 0.
+// Diagonal-block Cholesky: one cluster launch for 32 < b <= 256
+// (k_potf2_cluster); else (POSIT_POTF2=1) right-looking by 32-wide block
+// columns (leaf of <= 32 in one CTA, the rows below by the fused TRSM, the
+// trailing lower triangle by the one-thread-per-element SYRK), or
+// (POSIT_POTF2=0) the recursive potrf2 traversal.  Every stage is a no-op once
+// *info != 0.
 int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_base, cudaStream_t st) {
   if (b <= 0) return 0;
-  static const int mode = [] {                   // 1: blocked right-looking, 32-wide (default); 0: recursive
+  static const int mode = [] {  // 2: one cluster launch (default); 1: blocked right-looking, 32-wide; 0: recursive
     const char* e = getenv("POSIT_POTF2");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
-  if (mode == 1 && b <= 256) {
+  if (mode == 2 && b > TB && b <= PC_B) {
+    pb_count_launch();
+    k_potf2_cluster<<<PC_NC, 1024, 0, st>>>(A, lda, (int)b, info, row_base);
+    return last_launch();
+  }
+  if (mode >= 1 && b <= 256) {
     // right-looking by 32-wide block columns: leaf, the rows below by TRSM,
     // the trailing lower triangle by the one-thread-per-element SYRK
     for (int64_t j0 = 0; j0 < b; j0 += TB) {

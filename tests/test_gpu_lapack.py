@@ -149,6 +149,25 @@ def test_potrf_not_positive_definite_with_lookahead(cuda_ok):
     assert mismatch(np.tril(got)[:, :192], np.tril(ref)[:, :192]) == 0
 
 
+@pytest.mark.parametrize("fail_at,nb", [(0, 256), (37, 256), (250, 256), (255, 256), (100, 64), (70, 128)])
+def test_potrf_not_pd_inside_cluster_block(cuda_ok, fail_at, nb):
+    # the one-launch diagonal-block Cholesky (k_potf2_cluster, 32 < b <= 256) stops at
+    # the failing step in every CTA: info = k + 1, and inside the failing diagonal block
+    # every step before k is applied -- exactly the oracle's textbook loop there
+    n = 300
+    A = SI.config3(n)
+    A[fail_at, fail_at] = -2.0 * abs(A[fail_at, fail_at]) - 1.0
+    Ap = _pats(A)
+    ref, rinfo = O.potrf_lower(Ap)
+    got, info = _gpu_potrf(Ap, nb)
+    assert info == rinfo == fail_at + 1
+    s0 = (fail_at // nb) * nb
+    s1 = min(n, s0 + nb)
+    il = np.tril_indices(s1 - s0)
+    assert mismatch(got[s0:s1, s0:s1][il], ref[s0:s1, s0:s1][il]) == 0
+    assert mismatch(np.tril(got)[:, :s0], np.tril(ref)[:, :s0]) == 0
+
+
 @pytest.mark.parametrize("n", [1, 33, 300])
 def test_getrs_potrs_match_oracle(cuda_ok, n):
     import torch
