@@ -285,12 +285,10 @@ constexpr int FR_NMAX = 256;
 #define PG_RLTN_PIX 1
 #endif
 #if PG_RLTN_PIX
-#define FR_TPX0 tpx0
 #define FR_LW(x, E) ((uint32_t)(E) * 32u)
 #define FR_BW(x, E) ((uint32_t)(E) * 32u + tpx0)
 #define FR_LPAT(col, k) L[(int64_t)(col) * ldl + c0 + (k)]
 #else
-#define FR_TPX0 0u
 #define FR_LW(x, E) (x)
 #define FR_BW(x, E) (x)
 #define FR_LPAT(col, k) S.ld[k][col].w
@@ -314,89 +312,7 @@ struct FrSmem {
 #endif
 };
 
-// generic fallbacks of the in-block row solve, out of line (the solve is unrolled)
-__device__ __noinline__ uint32_t fr_sub_mul(uint32_t c, uint32_t a, uint32_t b) { return sub(c, mul(a, b)); }
-__device__ __noinline__ uint32_t fr_div(uint32_t a, uint32_t b) { return div(a, b); }
-
-// The in-block substitution of block J for ONE row in one thread (ROWIN, the
-// default): the row's W values stay in registers (three words each, see
-// PcVal in chol.cu's kernel; here a local copy), and after each division the
-// thread applies that final value to all later columns of the block
-// (right-looking: x_j <- x_j (-) l_jk (x) v_k for j > k, ascending k per
-// element, then x_j <- x_j (/) l_jj: Q6).  Every lane does useful work and
-// the divisions run on all rows at once, instead of W lanes per row of which
-// one divides and the others wait (FR_LANES below): about a sixth of the
-// in-block instructions for the same dependency chain.
-struct FrVal { uint32_t M; int32_t E; int32_t sg; };
-constexpr int32_t FR_PAT = 0x40000000;        // E marker: M holds the pattern (value outside the fast range)
-__device__ __forceinline__ FrVal fr_of(const LaneVal& v) {
-  return v.dec ? FrVal{v.a.M, v.a.E, v.a.sg} : FrVal{v.pat, FR_PAT, 1};
-}
-__device__ __forceinline__ LaneVal fr_lane(const FrVal& x) {
-  LaneVal v;
-  v.dec = x.E != FR_PAT;
-  v.a = pg::Acc{x.M, x.E, x.sg};
-  v.pat = x.M;
-  return v;
-}
-
 template <int W, int FR_ROWS>
-struct FrSmem;
-
-template <int W, int FR_ROWS, class Sm>
-__device__ __forceinline__ void fr_inblock_row(Sm& S, int r, int64_t rows, int c0, int jb, const pg::MacConst& K,
-                                               uint32_t tpx0) {
-  (void)tpx0;
-  const bool live = r < rows;
-  FrVal x[W];
-#pragma unroll
-  for (int c = 0; c < W; c++) {
-    LaneVal t;
-    lv_load(t, (live && c < jb) ? S.b[r][c0 + c] : 0u);
-    x[c] = fr_of(t);
-  }
-  bool allf = true;
-#pragma unroll
-  for (int k = 0; k < W; k++) {
-    if (k < jb) {
-      LaneVal v = fr_lane(x[k]);
-      const uint4 dv = S.ldiag[k];
-      bool done = false;
-      if (v.dec && dv.w != 0u) done = pg::acc_div(v.a, dv.x, (int32_t)dv.y, (int32_t)dv.z, S.ldrcp[k], K);
-      if (done) {
-        if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
-      } else {
-        lv_load(v, fr_div(lv_pattern(v), S.lblk[k][k]));
-      }
-      const uint32_t xp = lv_pattern(v);
-      const bool opf = lv_operand(v);
-      allf = allf && opf;
-      if (live) {
-        S.b[r][c0 + k] = xp;
-        // sign pre-negated: c (-) a b
-        S.bop[r][k] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), FR_BW(xp, (uint32_t)v.a.E));
-      }
-#pragma unroll
-      for (int j = k + 1; j < W; j++) {
-        if (j < jb) {
-          LaneVal t = fr_lane(x[j]);
-          const uint4 ad = S.lblkd[j][k];
-          if (ad.w != 0u && opf && t.dec) {
-            uint32_t bad = 0u;
-            pg::mac(t.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, v.a.M, v.a.E, -v.a.sg, K, bad);
-            if (!(t.a.E <= 75 && t.a.E >= -75) && t.a.E > -1000) { t.pat = pg::acc_encode(t.a); t.dec = false; }
-          } else {
-            lv_load(t, fr_sub_mul(lv_pattern(t), S.lblk[j][k], xp));
-          }
-          x[j] = fr_of(t);
-        }
-      }
-    }
-  }
-  S.rowfast[r] = allf ? 1 : 0;
-}
-
-template <int W, int FR_ROWS, bool ROWIN = true>
 __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
                                                                  int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
                                                                  int one) {
@@ -471,10 +387,6 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
       S.colfast[j] = f;
     }
     __syncthreads();
-    if constexpr (ROWIN) {
-      if (tid < FR_ROWS) fr_inblock_row<W, FR_ROWS>(S, tid, rows, c0, jb, K, FR_TPX0);
-    } else
-    // in-block substitution (FR_LANES): W lanes per row, lane = column
     // in-block substitution: W lanes per row, lane = column
     {
       const bool live = r < rows && c < jb;
@@ -632,36 +544,31 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   if (n <= FR_NMAX) {
     // one fused launch: each CTA solves FR_ROWS whole rows
     // variant: W lanes per row x FR_ROWS rows per CTA (env POSIT_RLTN = "W,ROWS")
-    // variant: W lanes per row x FR_ROWS rows per CTA, in-block solve by rows (1, default) or by lanes (0):
-    // env POSIT_RLTN = "W,ROWS[,INB]"
     static const int var = [] {
       const char* e = getenv("POSIT_RLTN");
-      int w = 16, r = 16, inb = 1;
-      if (e) sscanf(e, "%d,%d,%d", &w, &r, &inb);
-      return (inb ? 10000 : 0) + w * 100 + r;
+      int w = 16, r = 16;
+      if (e) sscanf(e, "%d,%d", &w, &r);
+      return w * 100 + r;
     }();
     static PbOncePerDevice attrs;
     pb_once_per_device(attrs, [] {
-      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16>));
-      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(FrSmem<16, 16>));
-      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 32>));
-      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<8, 16>));
-      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<8, 32>));
     });
     pb_count_launch();
-#define PB_RLTN(W_, R_, I_)                                                                                          \
-  k_trsm_rltn_fused<W_, R_, I_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(            \
-      L, ldl, B, ldb, m, n, stop, 1)
-    if (var == 11632) PB_RLTN(16, 32, true);
-    else if (var == 10816) PB_RLTN(8, 16, true);
-    else if (var == 10832) PB_RLTN(8, 32, true);
-    else if (var == 1616) PB_RLTN(16, 16, false);
-    else PB_RLTN(16, 16, true);
+#define PB_RLTN(W_, R_)                                                                                              \
+  k_trsm_rltn_fused<W_, R_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(L, ldl, B, ldb, m, \
+                                                                                                   n, stop, 1)
+    if (var == 1632) PB_RLTN(16, 32);
+    else if (var == 816) PB_RLTN(8, 16);
+    else if (var == 832) PB_RLTN(8, 32);
+    else PB_RLTN(16, 16);
 #undef PB_RLTN
     return last_launch();
   }

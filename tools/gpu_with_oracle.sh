@@ -11,7 +11,7 @@ export D=gpurun_out/$TAG
 mkdir -p $D
 nproc > $D/nproc.txt
 ls -la /tmp/oracle_ckpt > $D/ckpt_before.txt 2>&1
-OMP_NUM_THREADS=$(nproc) python tools/oracle_digests.py --configs $CFGS --out-dir $D/config_digests \
+OMP_NUM_THREADS=$(( $(nproc) - 1 )) nice -n 19 python tools/oracle_digests.py --configs $CFGS --out-dir $D/config_digests \
     --cache /tmp/oracle_cache --ckpt-dir /tmp/oracle_ckpt --time-budget $BUDGET > $D/oracle.log 2>&1 &
 OPID=$!
 bash $WORK > $D/work.log 2>&1
