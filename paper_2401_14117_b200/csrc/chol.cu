@@ -77,36 +77,36 @@ __global__ void __launch_bounds__(1024) k_potf2_leaf(uint32_t* A, int64_t lda, i
 
 // ---- the whole <= 256 x 256 diagonal block in ONE launch: a thread-block cluster --
 // Textbook right-looking loop (reading Q9) over all b columns, the lower
-// triangle distributed over the PC_NC CTAs of one cluster (distributed shared
-// memory; cluster barriers ~0.2 us instead of kernel launches or grid syncs):
-//   CTA c, warp w, lane l owns row i = l PC_NC + c, columns j = w + 32 q (q < 8),
-//   every element decoded in a register for the whole loop.
-// Step k: warp k % 32 owns column k.  Its lane k / 32 also keeps a redundant
-// copy of the diagonal chain d_k (every CTA keeps all of them: d_j <- d_j (-)
-// l_jk (x) l_jk, the same operations in the same order as the element a_jj,
-// hence the same bits), so every CTA takes l_kk = sqrt(d_k) itself and no
-// extra barrier is needed for it.  The warp divides its column-k elements by
-// l_kk (one posit division each) and pushes them into the column buffer of
-// every CTA of the cluster; one split cluster barrier per column publishes the
-// column, then every thread applies a_ij <- a_ij (-) l_ik (x) l_jk to its own
-// elements (ascending k per element: Q6).  A non-positive d_k stops every CTA
-// at the same step (info = row_base + k + 1, all steps < k applied, as the
-// oracle's loop).
-constexpr int PC_NC = 8;                       // CTAs per cluster (portable size)
-constexpr int PC_Q = 8;                        // column slots per thread
-constexpr int PC_B = 32 * PC_NC;               // 256: largest block
+// triangle distributed over the NC CTAs of one cluster (distributed shared
+// memory; a cluster barrier costs ~0.2 us, a kernel launch or grid sync
+// several): CTA c owns rows i = w NC + c, one row per warp w, lane l holds
+// columns j = l + 32 q (q < 8) of its row, decoded in registers for the whole
+// loop -- so the lower-triangle mask is nearly warp-uniform.
+// Iteration k: (1) thread k applies column k-1 to its copy of the diagonal
+// chain d_k (every CTA keeps all of them, thread j holding d_j: d_j <- d_j (-)
+// l_jk (x) l_jk, the operations of the element a_jj in its order, hence its
+// bits) and takes l_kk = sqrt(d_k), published in shared memory with a step
+// flag; (2) every thread applies column k-1 to its own elements (ascending k
+// per element: Q6); (3) lane k % 32 of every row warp divides its column-k
+// element by l_kk (one posit division) and pushes it into the column buffer of
+// every CTA; (4) one split cluster barrier per column.  A non-positive d_k
+// stops every CTA at the same step (info = row_base + k + 1, every step < k
+// applied, as the oracle's loop).
+constexpr int PC_Q = 8;                        // column slots per lane
+constexpr int PC_B = 256;                      // largest block
 
 struct PcSmem {
   uint32_t colp[2][PC_B];                      // column k: patterns l_jk (rows j > k)
   uint4 cola[2][PC_B];                         // A-format decode {M, E, sigma, fast}
   uint4 colb[2][PC_B];                         // B-format decode {M, E, sg, fast}
   int fail;
+  int lkk_step;                                // the step whose l_kk is in lkk
+  uint32_t lkk;
   uint4 tp[pg::TSIZE], tx[pg::TSIZE];          // the MAC's per-scale constant tables
 };
 
-// A LaneVal in three registers (the kernel keeps nine per thread under the
-// 64-register cap of 1024-thread CTAs): decoded {M, E, sg}, or the pattern in
-// M with E = PC_PAT when the value is outside the fast range.
+// A LaneVal in three registers: decoded {M, E, sg}, or the pattern in M with
+// E = PC_PAT when the value is outside the fast range.
 constexpr int32_t PC_PAT = 0x40000000;
 struct PcVal { uint32_t M; int32_t E; int32_t sg; };
 
@@ -120,81 +120,95 @@ __device__ __forceinline__ LaneVal pc_lane(const PcVal& x) {
   v.pat = x.M;
   return v;
 }
+__device__ __forceinline__ PcVal pc_load(uint32_t x) {
+  LaneVal t;
+  lv_load(t, x);
+  return pc_of(t);
+}
+
+// x <- x (-) l_ik (x) l_jk with the column buffer's entries (fast MAC, generic fallback)
+__device__ __forceinline__ void pc_fms(PcVal& x, const PcSmem& S, int q, int i, int j, const pg::MacConst& K) {
+  const uint4 ad = S.cola[q][i], bd = S.colb[q][j];
+  LaneVal t = pc_lane(x);
+  lv_fms_t(t, S.colp[q][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, S.colp[q][j], K);
+  x = pc_of(t);
+}
 
 __device__ __forceinline__ void pc_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void pc_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
-__global__ void __cluster_dims__(PC_NC, 1, 1) __launch_bounds__(1024, 1)
+template <int NC>
+__global__ void __launch_bounds__(32 * (PC_B / NC), 1)
     k_potf2_cluster(uint32_t* A, int64_t lda, int b, int32_t* info, int64_t row_base) {
   namespace cg = cooperative_groups;
+  constexpr int NT = 32 * (PC_B / NC);                          // one warp per row of this CTA
   __shared__ PcSmem S;
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int i = l * PC_NC + c;                                  // my row
-  const bool stop0 = *info != 0;                                // an earlier block failed: every CTA returns
-  if (stop0) return;
-  pg::fill_tables(S.tp, S.tx, threadIdx.x, 1024);
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int i = w * NC + c;                                     // my row
+  if (*info != 0) return;                                       // an earlier block failed: every CTA returns
+  pg::fill_tables(S.tp, S.tx, tid, NT);
   pg::MacConst K;
   K.one = 1u; K.sixteen = 16u;
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
-  if (threadIdx.x == 0) S.fail = 0;
+  if (tid == 0) { S.fail = 0; S.lkk_step = -1; }
   PcVal v[PC_Q];
 #pragma unroll
   for (int q = 0; q < PC_Q; q++) {
-    const int j = w + 32 * q;
-    LaneVal t;
-    lv_load(t, (i < b && j <= i) ? A[(int64_t)i * lda + j] : 0u);
-    v[q] = pc_of(t);
+    const int j = l + 32 * q;
+    v[q] = pc_load((i < b && j <= i) ? A[(int64_t)i * lda + j] : 0u);
   }
-  PcVal dd;                                                     // redundant diagonal d_j, j = w + 32 l (l < 8)
-  const int jd = w + 32 * l;
-  {
-    LaneVal t;
-    lv_load(t, (l < PC_Q && jd < b) ? A[(int64_t)jd * lda + jd] : 0u);
-    dd = pc_of(t);
-  }
+  PcVal dd = pc_load(tid < b ? A[(int64_t)tid * lda + tid] : 0u);   // d_j, j = tid
   __syncthreads();
   cl.sync();                                                    // every CTA running before any remote store
+  volatile int* vstep = &S.lkk_step;
   bool failed = false;
   for (int k = 0; k < b; k++) {
     const int qk = k & 1, qp = qk ^ 1;
     if (k > 0) {
       pc_wait();                                                // column k - 1 published everywhere
       if (S.fail) { failed = true; break; }                     // same step in every CTA: barriers stay balanced
-      // this step's critical chain first: my diagonal copy and my column-k element
-      if (l < PC_Q && jd >= k && jd < b) {
-        const uint4 ad = S.cola[qp][jd], bd = S.colb[qp][jd];
-        LaneVal d = pc_lane(dd);
-        lv_fms_t(d, S.colp[qp][jd], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, S.colp[qp][jd], K);
-        dd = pc_of(d);
-      }
     }
-    if (w == (k & 31)) {                                        // my warp owns column k
-      const int qc = k >> 5;                                    // its slot (selected, not indexed: no local memory)
-      PcVal xs = v[0];
-#pragma unroll
-      for (int q = 1; q < PC_Q; q++)
-        if (q == qc) xs = v[q];
-      LaneVal x = pc_lane(xs);
-      if (k > 0 && i < b && i >= k) {                           // step k - 1's update of my column-k element
-        const uint4 ad = S.cola[qp][i], bd = S.colb[qp][k];
-        lv_fms_t(x, S.colp[qp][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u, S.colp[qp][k], K);
-      }
-      // l_kk = sqrt(d_k) in lane k / 32, broadcast to the warp
-      uint32_t dk = 0u;
-      if (l == qc) dk = lv_pattern(pc_lane(dd));
-      dk = __shfl_sync(0xFFFFFFFFu, dk, qc);
-      if ((int32_t)dk <= 0) {                                   // zero, negative or NaR pivot: stop
-        if (l == 0) {
+    // (1) the diagonal chain and l_kk
+    if (tid < b && tid >= k) {
+      if (k > 0) pc_fms(dd, S, qp, tid, tid, K);
+      if (tid == k) {
+        const uint32_t dk = lv_pattern(pc_lane(dd));
+        if ((int32_t)dk <= 0) {                                 // zero, negative or NaR pivot: stop
           S.fail = 1;
           if (c == 0) *info = (int32_t)(row_base + k + 1);
+        } else {
+          S.lkk = p32::sqrt(dk);
         }
-      } else {
-        const uint32_t lkk = p32::sqrt(dk);
-        if (i == k) lv_load(x, lkk);
-        if (i > k && i < b) {
+        __threadfence_block();
+        *vstep = k;
+      }
+    }
+    // (2) column k - 1 on my elements (the column-k slot is the first active one)
+    if (k > 0 && i < b) {
+#pragma unroll
+      for (int q = 0; q < PC_Q; q++) {
+        const int j = l + 32 * q;
+        if (j >= k && j <= i) pc_fms(v[q], S, qp, i, j, K);
+      }
+    }
+    // (3) my row's column-k element: divide by l_kk and publish it to every CTA
+    if (l == (k & 31) && i >= k && i < b) {
+      while (*vstep != k) { }
+      __threadfence_block();
+      if (!S.fail) {
+        const uint32_t lkk = S.lkk;
+        const int qc = k >> 5;
+        PcVal xs = v[0];
+#pragma unroll
+        for (int q = 1; q < PC_Q; q++)
+          if (q == qc) xs = v[q];
+        LaneVal x = pc_lane(xs);
+        if (i == k) {
+          lv_load(x, lkk);
+        } else {
           pg::Acc dv;
           const bool dok = pg::acc_decode(lkk, dv) && dv.E <= 37 && dv.E >= -37;
           bool done = false;
@@ -212,38 +226,25 @@ __global__ void __cluster_dims__(PC_NC, 1, 1) __launch_bounds__(1024, 1)
           const uint4 bv = lv_operand(x) ? make_uint4(x.a.M, (uint32_t)x.a.E, (uint32_t)x.a.sg, 1u)
                                          : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-          for (int r = 0; r < PC_NC; r++) {                     // push l_ik into every CTA's column buffer
+          for (int r = 0; r < NC; r++) {                        // push l_ik into every CTA's column buffer
             *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
             *cl.map_shared_rank(&S.cola[qk][i], r) = av;
             *cl.map_shared_rank(&S.colb[qk][i], r) = bv;
           }
         }
-      }
-      xs = pc_of(x);
+        xs = pc_of(x);
 #pragma unroll
-      for (int q = 0; q < PC_Q; q++)
-        if (q == qc) v[q] = xs;
-    }
-    // the rest of step k - 1's updates on my elements (columns j > k)
-    if (k > 0) {
-#pragma unroll
-      for (int q = 0; q < PC_Q; q++) {
-        const int j = w + 32 * q;
-        if (j > k && j <= i && i < b) {
-          const uint4 ad = S.cola[qp][i], bd = S.colb[qp][j];
-          LaneVal t = pc_lane(v[q]);
-          lv_fms_t(t, S.colp[qp][i], ad.w != 0u, ad, bd.x, (int32_t)bd.y, (int32_t)bd.z, bd.w != 0u,
-                   S.colp[qp][j], K);
-          v[q] = pc_of(t);
-        }
+        for (int q = 0; q < PC_Q; q++)
+          if (q == qc) v[q] = xs;
       }
     }
+    __syncwarp();
     pc_arrive();                                                // my pushes for column k (release)
   }
   if (!failed) pc_wait();                                       // the last arrive (a failure already waited)
 #pragma unroll
   for (int q = 0; q < PC_Q; q++) {
-    const int j = w + 32 * q;
+    const int j = l + 32 * q;
     if (i < b && j <= i) A[(int64_t)i * lda + j] = lv_pattern(pc_lane(v[q]));
   }
   cl.sync();                                                    // no CTA exits while others may still read it
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(256) k_syrk_tiny(int64_t n, int64_t k, const u
 }
 
 // Diagonal-block Cholesky: one cluster launch for 32 < b <= 256
-// (k_potf2_cluster); else (POSIT_POTF2=1) right-looking by 32-wide block
+// (k_potf2_cluster, POSIT_POTF2=2); else (POSIT_POTF2=1) right-looking by 32-wide block
 // columns (leaf of <= 32 in one CTA, the rows below by the fused TRSM, the
 // trailing lower triangle by the one-thread-per-element SYRK), or
 // (POSIT_POTF2=0) the recursive potrf2 traversal.  Every stage is a no-op once
@@ -337,9 +338,32 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     return e ? atoi(e) : 2;
   }();
   if (mode == 2 && b > TB && b <= PC_B) {
+    // POSIT_POTF2_NC: CTAs per cluster, 8 (portable; 32 row warps per CTA) or 16 (16 row warps)
+    static const int nc = [] {
+      const char* e = getenv("POSIT_POTF2_NC");
+      return (e && atoi(e) == 16) ? 16 : 8;
+    }();
+    static PbOncePerDevice attrs;
+    pb_once_per_device(attrs, [] {
+      cudaFuncSetAttribute(k_potf2_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
     pb_count_launch();
-    k_potf2_cluster<<<PC_NC, 1024, 0, st>>>(A, lda, (int)b, info, row_base);
-    return last_launch();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nc);
+    cfg.blockDim = dim3(32 * (PC_B / nc));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int32_t bb = (int32_t)b;
+    const cudaError_t e = nc == 16 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base)
+                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base);
+    return e == cudaSuccess ? 0 : POSIT_ECUDA;
   }
   if (mode >= 1 && b <= 256) {
     // right-looking by 32-wide block columns: leaf, the rows below by TRSM,

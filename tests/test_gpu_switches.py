@@ -104,6 +104,7 @@ LAPACK_SWITCHES = [
     {"POSIT_RLTN": "16,32"},
     {"POSIT_POTF2": "0"},
     {"POSIT_POTF2": "1"},
+    {"POSIT_POTF2_NC": "16"},
     {"POSIT_GEMM_VARIANT": "12", "POSIT_GEMM_TINY": "2"},
     {"POSIT_GEMM_VARIANT": "13"},
     {"POSIT_GEMM_VARIANT": "14"},
