@@ -291,13 +291,18 @@ constexpr int FR_NMAX = 256;
 #else
 #define FR_LW(x, E) (x)
 #define FR_BW(x, E) (x)
-#define FR_LPAT(col, k) S.ld[k][col].w
+#define FR_LPAT(col, k) S.ld[k][(col) - ch0].w
 #endif
 
-template <int W, int FR_ROWS>
+// CH: the later columns' L values are staged (and the update loop run) in
+// chunks of CH columns; CH < FR_NMAX halves the shared memory (with the
+// in-block MAC's product table computed in registers instead of read from
+// shared memory) so that three CTAs fit an SM.
+template <int W, int FR_ROWS, int CH = FR_NMAX>
 struct FrSmem {
+  static constexpr bool TP = CH == FR_NMAX;   // the in-block MAC's product table in shared memory
   uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
-  uint4 ld[W][FR_NMAX];                       // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
+  uint4 ld[W][CH];                            // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
   uint4 bop[FR_ROWS][W];                      // block J's final values, B-format {M, E, sg (0: slow), pattern}
   uint32_t lblk[W][W + 1];                    // L's diagonal block J (patterns)
   uint4 lblkd[W][W];                          // the same, decoded A-format {M, E, sigma, fast}
@@ -305,30 +310,31 @@ struct FrSmem {
   double ldrcp[W];                            // RN(2^32 / M) of each diagonal divisor
   int colfast[FR_NMAX];                       // column j's staged L values all fast-path operands
   int rowfast[FR_ROWS];                       // row r's block-J values all fast-path operands
-  uint4 tp[pg::TSIZE];                        // the MAC's per-scale constant tables
+  uint4 tp[TP ? pg::TSIZE : 1];              // the MAC's per-scale constant tables
   uint4 tx[pg::TSIZE];
 #if PG_RLTN_PIX
   uint4 tpx[pg::PIX_NE];                      // the PIX product table of the update loop
 #endif
 };
 
-template <int W, int FR_ROWS>
-__global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
-                                                                 int64_t ldb, int64_t m, int64_t n, const int32_t* stop,
-                                                                 int one) {
+template <int W, int FR_ROWS, int CH = FR_NMAX, int MINB = 2>
+__global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
+                                                                    int64_t ldb, int64_t m, int64_t n,
+                                                                    const int32_t* stop, int one) {
   constexpr int NT = FR_ROWS * W;
+  using Sm = FrSmem<W, FR_ROWS, CH>;
   extern __shared__ __align__(16) unsigned char fr_raw[];
-  FrSmem<W, FR_ROWS>& S = *reinterpret_cast<FrSmem<W, FR_ROWS>*>(fr_raw);
+  Sm& S = *reinterpret_cast<Sm*>(fr_raw);
   if (stop != nullptr && *stop != 0) return;
   const int tid = threadIdx.x;
   const int r = tid / W, c = tid % W;                  // row of the tile, column within a block
   const int grp = (tid & 31) & ~(W - 1);               // first lane of this row's lane group
   const int64_t r0 = (int64_t)blockIdx.x * FR_ROWS;
   const int64_t rows = (m - r0) < FR_ROWS ? (m - r0) : FR_ROWS;
-  pg::fill_tables(S.tp, S.tx, tid, NT);
+  pg::fill_tables<(PG_PROD_BY_SUM != 0), Sm::TP>(S.tp, S.tx, tid, NT);
   pg::MacConst K;
   K.one = (uint32_t)one; K.sixteen = 16u * K.one;
-  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + pg::TBIAS);
+  K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + (Sm::TP ? pg::TBIAS : 0));
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
 #if PG_RLTN_PIX
   pg::fill_prod_pix<false>(S.tpx, tid, NT);
@@ -361,8 +367,11 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
       }
     }
     const int nrest = (int)n - c0 - jb;
-    for (int jj = tid; jj < nrest; jj += NT) {            // thread per column j: its jb values are contiguous
-      const int j = c0 + jb + jj;
+    // stage the L values of the later columns [ch0, ch0 + CH) (thread per column: its jb values are contiguous)
+    auto stage_chunk = [&](int ch0) {
+    const int nch = ((int)n - ch0) < CH ? ((int)n - ch0) : CH;
+    for (int jj = tid; jj < nch; jj += NT) {
+      const int j = ch0 + jj;
       int f = 1;
       if (jb == W) {                                      // full block: all W loads in flight together
         uint32_t xs[W];
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
         for (int k = 0; k < W; k++) {
           uint4 d;
           const bool fk = fast_a(xs[k], d);
-          S.ld[k][j] = make_uint4(d.x, d.y, d.z, FR_LW(xs[k], d.y));
+          S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(xs[k], d.y));
           f &= (int)fk;
         }
       } else {
@@ -380,12 +389,14 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
           const uint32_t x = L[(int64_t)j * ldl + c0 + k];
           uint4 d;
           const bool fk = fast_a(x, d);
-          S.ld[k][j] = make_uint4(d.x, d.y, d.z, FR_LW(x, d.y));
+          S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(x, d.y));
           f &= (int)fk;
         }
       }
       S.colfast[j] = f;
     }
+    };
+    if (nrest > 0) stage_chunk(c0 + jb);
     __syncthreads();
     // in-block substitution: W lanes per row, lane = column
     {
@@ -415,7 +426,8 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
           const uint4 ad = S.lblkd[c][k];
           if (ad.w != 0u && bfk && v.dec) {
             uint32_t bad = 0u;
-            pg::mac(v.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bs, K, bad);
+            if constexpr (Sm::TP) pg::mac(v.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bs, K, bad);
+            else pg::mac(v.a, ad.x, (int32_t)ad.y, (int32_t)ad.z, bM, bE, -bs, pg::CalcConst(), bad);
             if (!(v.a.E <= 75 && v.a.E >= -75) && v.a.E > -1000) { v.pat = pg::acc_encode(v.a); v.dec = false; }
           } else {
             pg::Acc bk{bM, bE, bs};
@@ -442,17 +454,24 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
     // (|Ep| <= 75, |E| grows by <= 1 per step, cancellation stops at >= -106).
     // Four of the thread's columns are advanced together (independent chains
     // for ILP); a group with any slow column runs the generic path.
+    for (int ch0 = c0 + jb; ch0 < (int)n; ch0 += CH) {
+    const int chend = ((int)n - ch0) < CH ? (int)n : ch0 + CH;
+    if (ch0 > c0 + jb) {                                  // the next chunk of L (the previous one is done)
+      __syncthreads();
+      stage_chunk(ch0);
+      __syncthreads();
+    }
     if (r < rows) {
       const bool rf = S.rowfast[r] != 0;
       constexpr int G = 4;
-      for (int col0 = c0 + jb + c; col0 < (int)n; col0 += G * W) {
+      for (int col0 = ch0 + c; col0 < chend; col0 += G * W) {
         pg::Acc a[G];
         uint32_t x[G];
         bool ok = rf;
 #pragma unroll
         for (int u = 0; u < G; u++) {
           const int col = col0 + u * W;
-          const bool in = col < (int)n;
+          const bool in = col < chend;
           x[u] = in ? S.b[r][col] : 0u;
           const bool d = pg::acc_decode(x[u], a[u]) && (x[u] == 0u || (a[u].E <= 75 && a[u].E >= -75));
           ok = ok && d && (!in || S.colfast[col] != 0);
@@ -464,7 +483,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
             const uint4 bd = S.bop[r][k];
 #pragma unroll
             for (int u = 0; u < G; u++) {
-              const uint4 ad = S.ld[k][min(col0 + u * W, (int)n - 1)];
+              const uint4 ad = S.ld[k][min(col0 + u * W, chend - 1) - ch0];
 #if PG_RLTN_PIX
               pg::mac<pg::MacConst, true, false, false, false, true>(a[u], ad.x, (int32_t)ad.y, (int32_t)ad.z, bd.x,
                                                                       (int32_t)bd.y, (int32_t)bd.z, K, bad, ad.w, bd.w);
@@ -475,18 +494,19 @@ __global__ void __launch_bounds__(FR_ROWS * W, 2) k_trsm_rltn_fused(const uint32
           }
 #pragma unroll
           for (int u = 0; u < G; u++)
-            if (col0 + u * W < (int)n) S.b[r][col0 + u * W] = pg::acc_encode(a[u]);
+            if (col0 + u * W < chend) S.b[r][col0 + u * W] = pg::acc_encode(a[u]);
         } else {
 #pragma unroll 1
           for (int u = 0; u < G; u++) {
             const int col = col0 + u * W;
-            if (col >= (int)n) break;
+            if (col >= chend) break;
             uint32_t y = x[u];
             for (int k = 0; k < jb; k++) y = sub(y, mul(FR_LPAT(col, k), S.b[r][c0 + k]));
             S.b[r][col] = y;
           }
         }
       }
+    }
     }
   }
   __syncthreads();
@@ -544,16 +564,20 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
   if (n <= FR_NMAX) {
     // one fused launch: each CTA solves FR_ROWS whole rows
     // variant: W lanes per row x FR_ROWS rows per CTA (env POSIT_RLTN = "W,ROWS")
+    // variant: W lanes per row x FR_ROWS rows per CTA [x L staged in chunks of CH columns]:
+    // env POSIT_RLTN = "W,ROWS[,CH]"; CH = 128 fits three CTAs per SM
     static const int var = [] {
       const char* e = getenv("POSIT_RLTN");
-      int w = 16, r = 16;
-      if (e) sscanf(e, "%d,%d", &w, &r);
-      return w * 100 + r;
+      int w = 16, r = 16, ch = 256;
+      if (e) sscanf(e, "%d,%d,%d", &w, &r, &ch);
+      return (ch == 128 ? 100000 : 0) + w * 100 + r;
     }();
     static PbOncePerDevice attrs;
     pb_once_per_device(attrs, [] {
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16, 128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 16, 128>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 32>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -562,12 +586,15 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
                            (int)sizeof(FrSmem<8, 32>));
     });
     pb_count_launch();
-#define PB_RLTN(W_, R_)                                                                                              \
-  k_trsm_rltn_fused<W_, R_><<<(unsigned)((m + R_ - 1) / R_), R_ * W_, sizeof(FrSmem<W_, R_>), st>>>(L, ldl, B, ldb, m, \
-                                                                                                   n, stop, 1)
+#define PB_RLTN(W_, R_, ...)                                                                                         \
+  k_trsm_rltn_fused<W_, R_, ##__VA_ARGS__><<<(unsigned)((m + R_ - 1) / R_), R_ * W_,                              \
+                                              sizeof(FrSmem<W_, R_, ##__VA_ARGS__>), st>>>(L, ldl, B, ldb, m, n, stop, 1)
     if (var == 1632) PB_RLTN(16, 32);
     else if (var == 816) PB_RLTN(8, 16);
     else if (var == 832) PB_RLTN(8, 32);
+    else if (var == 101616) k_trsm_rltn_fused<16, 16, 128, 3><<<(unsigned)((m + 15) / 16), 256,
+                                                               sizeof(FrSmem<16, 16, 128>), st>>>(L, ldl, B, ldb, m,
+                                                                                                  n, stop, 1);
     else PB_RLTN(16, 16);
 #undef PB_RLTN
     return last_launch();

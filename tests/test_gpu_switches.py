@@ -102,6 +102,7 @@ LAPACK_SWITCHES = [
     {"POSIT_LLNU_COL": "8"},
     {"POSIT_RLTN": "8,16"},
     {"POSIT_RLTN": "16,32"},
+    {"POSIT_RLTN": "16,16,128"},
     {"POSIT_POTF2": "0"},
     {"POSIT_POTF2": "1"},
     {"POSIT_POTF2_NC": "16"},
