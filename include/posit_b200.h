@@ -241,7 +241,21 @@ int posit_to_f64(const uint32_t* p, double* out, int64_t count, void* stream);
 #define POSIT_OP_MUL 2
 #define POSIT_OP_DIV 3
 #define POSIT_OP_SQRT 4
+/* The same add and mul computed by the binary64-pipe MAC's steps (the D-MAC,
+ * DESIGN.md section 6): 5 = add (operands |scale| <= 75, else the generic add),
+ * 6 = mul (operands |scale| <= 37, else the generic mul).  Same bits as 0 / 2:
+ * they exist so the D-MAC's rounding can be checked against the oracle one
+ * operation at a time (every product and every sum rounded). */
+#define POSIT_OP_DADD 5
+#define POSIT_OP_DMUL 6
 int posit_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream);
+
+/* out[i] = c[i] (+) (a[i] (x) b[i]): one step of the trailing update's chain
+ * (reading Q6), through the D-MAC when |Ea|, |Eb| <= 37 and
+ * |Ec| <= 91 (nonzero operands), else the generic mul and add (same bits).
+ * Device pointers, count elements each; stream-ordered. */
+int posit_vec_dmac(const uint32_t* c, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -19,13 +19,13 @@ import os
 __all__ = [
     "lib", "PositError", "posit_gemm", "posit_gemm_eq2", "posit_gemm_naive", "posit_gemm_host", "posit_syrk", "posit_trsm",
     "posit_getrf", "posit_getrf_panel", "posit_getrs", "posit_potrs", "posit_laswp", "posit_potrf", "posit_from_f64", "posit_to_f64",
-    "posit_vec_op", "posit_iamax_key", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
+    "posit_vec_op", "posit_vec_dmac", "posit_iamax_key", "posit_kernel_launches", "POSIT_ONE", "POSIT_MONE", "POSIT_NAR", "OPS",
 ]
 
 POSIT_ONE = 0x40000000
 POSIT_MONE = 0xC0000000
 POSIT_NAR = 0x80000000
-OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "dadd": 5, "dmul": 6}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("POSIT_LIB_PATH") or os.path.join(_HERE, "libposit_b200.so")
@@ -69,6 +69,7 @@ def lib() -> ctypes.CDLL:
         L.posit_from_f64.argtypes = [vp, vp, i64, vp]
         L.posit_to_f64.argtypes = [vp, vp, i64, vp]
         L.posit_vec_op.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp]
+        L.posit_vec_dmac.argtypes = [vp, vp, vp, vp, i64, vp]
         L.posit_kernel_launches.restype = ctypes.c_uint64
         L.posit_strerror.argtypes = [ctypes.c_int]
         L.posit_strerror.restype = ctypes.c_char_p
@@ -324,4 +325,17 @@ def posit_vec_op(op: str, a, b=None, out=None, stream=None):
     _vec(out, "out", torch.int32, a.numel())
     _check(lib().posit_vec_op(OPS[op], _ptr(a), _ptr(a if b is None else b), _ptr(out), a.numel(), _stream(stream)),
            "posit_vec_op")
+    return out
+
+
+def posit_vec_dmac(c, a, b, out=None, stream=None):
+    """out = c (+) (a (x) b) elementwise through the binary64-pipe MAC (posit_vec_dmac)."""
+    import torch
+    _vec(c, "c", torch.int32, 0)
+    _vec(a, "a", torch.int32, c.numel())
+    _vec(b, "b", torch.int32, c.numel())
+    if out is None:
+        out = torch.empty_like(c)
+    _vec(out, "out", torch.int32, c.numel())
+    _check(lib().posit_vec_dmac(_ptr(c), _ptr(a), _ptr(b), _ptr(out), c.numel(), _stream(stream)), "posit_vec_dmac")
     return out

@@ -11,6 +11,9 @@ namespace pg { struct Params; }
 // pdl: programmatic dependent launch after the previous kernel on st (only for
 // an update that does not read that kernel's output)
 int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl = false);
+int pb_launch_gemm_d(const pg::Params& P, bool transb, bool syrk, cudaStream_t st, bool pdl, int variant);   // gemm_d.cu
+int pb_vec_d(int op, const uint32_t* a, const uint32_t* b, const uint32_t* c, uint32_t* out, int64_t count,
+             cudaStream_t st);
 int pb_launch_gemm_naive(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);
 int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st);   // chol.cu
 

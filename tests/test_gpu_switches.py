@@ -6,7 +6,8 @@ subprocess on the same inputs; the parent compares its outputs word by word
 with the CPU oracle.  By the order contract (reading Q6) every switch changes
 only the traversal, so all of them must give the oracle's bits:
 
-* GEMM: POSIT_GEMM_VARIANT 11..14 (the four tile configurations G1..G4) x
+* GEMM: POSIT_GEMM_VARIANT 11..14 (the integer-MAC tiles G1..G4), 21..24 (the
+  binary64-pipe tiles D1..D4) and POSIT_GEMM_PATH=0 (integer MAC by default) x
   {NN, NT, TN, SYRK} at a shape above the one-thread-per-output cutoff with
   ragged tails in m, n and k, plus the default model choice and the tiny-kernel
   routes (POSIT_GEMM_TINY = 0 / 2);
@@ -64,7 +65,9 @@ def gemm_case():
 
 
 GEMM_VARIANTS = [{}, {"POSIT_GEMM_VARIANT": "11"}, {"POSIT_GEMM_VARIANT": "12"}, {"POSIT_GEMM_VARIANT": "13"},
-                 {"POSIT_GEMM_VARIANT": "14"}, {"POSIT_GEMM_TINY": "0"}]
+                 {"POSIT_GEMM_VARIANT": "14"}, {"POSIT_GEMM_TINY": "0"}, {"POSIT_GEMM_PATH": "0"},
+                 {"POSIT_GEMM_VARIANT": "21"}, {"POSIT_GEMM_VARIANT": "22"}, {"POSIT_GEMM_VARIANT": "23"},
+                 {"POSIT_GEMM_VARIANT": "24"}, {"POSIT_GEMM_VARIANT": "22", "POSIT_GEMM_TINY": "0"}]
 
 
 @pytest.mark.parametrize("env", GEMM_VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
@@ -109,6 +112,8 @@ LAPACK_SWITCHES = [
     {"POSIT_GEMM_VARIANT": "12", "POSIT_GEMM_TINY": "2"},
     {"POSIT_GEMM_VARIANT": "13"},
     {"POSIT_GEMM_VARIANT": "14"},
+    {"POSIT_GEMM_PATH": "0"},
+    {"POSIT_GEMM_PATH": "0", "POSIT_LOOKAHEAD": "0"},
 ]
 
 

@@ -66,6 +66,52 @@ double run(const char* name, int per_instr, unsigned* out, long long* cyc, int n
   printf("  \"%s\": %.3f%s\n", name, rate, last ? "" : ",");
   return rate;
 }
+
+// binary64 pipe: CH independent chains of real double registers per thread
+template <int OP>
+__global__ void kernd(unsigned* out, unsigned seed, long long* cyc) {
+  double r[CH];
+  unsigned q[CH];
+  for (int i = 0; i < CH; i++) { r[i] = 1.0 + 1e-9 * (seed * (threadIdx.x + 1) + i); q[i] = seed * (threadIdx.x + 1) + i; }
+  const double b = 1.0000001, c = -0.5e-7;
+  const unsigned ib = seed ^ 0x1234567u, ic = seed + 77u;
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+      if (OP == 0) asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(c));
+      if (OP == 1) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(r[i]) : "d"(b), "d"(c));
+      if (OP == 2) asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(b));
+      if (OP == 3) asm volatile("add.rm.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(c));
+      if (OP == 4) { asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(c));
+                     asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(q[i]) : "r"(ib), "r"(ic)); }
+      if (OP == 5) { asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(c));
+                     asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(q[i]) : "r"(ib), "r"(ic)); }
+      if (OP == 6) { asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[i]) : "d"(c));
+                     asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(q[i]) : "r"(ib), "r"(ic));
+                     asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(q[i]) : "r"(ib), "r"(ic)); }
+    }
+  }
+  long long t1 = clock64();
+  double acc = 0; unsigned u = 0;
+  for (int i = 0; i < CH; i++) { acc += r[i]; u ^= q[i]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (unsigned)__double2loint(acc) ^ u;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int OP>
+double rund(const char* name, int per_instr, unsigned* out, long long* cyc, int nsm, bool last) {
+  const int threads = 1024, blocks = nsm * 2;
+  kernd<OP><<<blocks, threads>>>(out, 3u, cyc);
+  cudaDeviceSynchronize();
+  long long h[4096];
+  cudaMemcpy(h, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+  double mx = 0;
+  for (int i = 0; i < blocks; i++) mx = h[i] > mx ? h[i] : mx;
+  double rate = 2.0 * 32 * ITERS * CH * per_instr / mx;
+  printf("  \"%s\": %.3f%s\n", name, rate, last ? "" : ",");
+  return rate;
+}
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   unsigned* out; long long* cyc;
@@ -94,7 +140,14 @@ int main() {
   run<22>("fma.rn.f64 (DFMA)", 1, out, cyc, nsm, false);
   run<23>("popc (POPC)", 1, out, cyc, nsm, false);
   run<24>("add.u32 imm (VIADD?)", 1, out, cyc, nsm, false);
-  run<25>("setp+selp+or", 3, out, cyc, nsm, true);
+  run<25>("setp+selp+or", 3, out, cyc, nsm, false);
+  rund<0>("f64 add.rn (DADD)", 1, out, cyc, nsm, false);
+  rund<1>("f64 fma.rn (DFMA)", 1, out, cyc, nsm, false);
+  rund<2>("f64 mul.rn (DMUL)", 1, out, cyc, nsm, false);
+  rund<3>("f64 add.rm (DADD.RM)", 1, out, cyc, nsm, false);
+  rund<4>("DADD + LOP3 (1:1)", 2, out, cyc, nsm, false);
+  rund<5>("DADD + IMAD (1:1)", 2, out, cyc, nsm, false);
+  rund<6>("DADD + LOP3 + IMAD (1:1:1)", 3, out, cyc, nsm, true);
   printf("}\n");
   return 0;
 }
