@@ -498,7 +498,7 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st,
   // the binary64-pipe MAC (gemm_d.cu) unless POSIT_GEMM_PATH=0 or an integer-MAC tile is forced (11..14)
   static const int path_env = [] {
     const char* e = getenv("POSIT_GEMM_PATH");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   if ((path_env != 0 && (v == 0 || v >= 21)) || v >= 21) return pb_launch_gemm_d(P, transb, syrk, st, pdl, v);
   if (v == 0) {

@@ -38,7 +38,7 @@ struct CfgD {
     double b[2][BK][BN];
     uint32_t ra[BM * BK];             // raw patterns of the next slab (cp.async target, by quad)
     uint32_t rb[BK * BN];
-    double tab[pgd::DT_SIZE];         // M(E) by hi word >> 20
+    pgd::dtab_t tab[pgd::DT_SIZE];    // M(E) by biased exponent
   };
 };
 
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
   if (P.stop != nullptr && *P.stop != 0) return;
 
   const uint32_t flip = P.neg ? 1u : 0u;
-  for (int i = tid; i < pgd::DT_SIZE; i += NTHR) S.tab[i] = pgd::dtab_entry(i);   // visible after the first barrier
+  for (int i = tid; i < pgd::DT_SIZE; i += NTHR) S.tab[i] = pgd::dtab_fill(i);   // visible after the first barrier
   const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(S.tab);
 
   double acc[TM][TN];
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 // operands inside their fast range; outside it the generic ops (same bits).
 __global__ void k_vec_d(int op, const uint32_t* a, const uint32_t* b, const uint32_t* c, uint32_t* out,
                         int64_t count) {
-  __shared__ double tab[pgd::DT_SIZE];
-  for (int i = threadIdx.x; i < pgd::DT_SIZE; i += blockDim.x) tab[i] = pgd::dtab_entry(i);
+  __shared__ pgd::dtab_t tab[pgd::DT_SIZE];
+  for (int i = threadIdx.x; i < pgd::DT_SIZE; i += blockDim.x) tab[i] = pgd::dtab_fill(i);
   __syncthreads();
   const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {

@@ -41,7 +41,16 @@
 
 namespace pgd {
 
-constexpr int DT_SIZE = 4096;        // table entries: indexed by the hi word >> 20 (sign | biased exponent)
+// Table entries are indexed by the biased exponent (hi word >> 20, sign masked
+// off): one entry per binade for both signs, so a warp whose lanes hold values
+// of either sign reads one address per binade (with the sign in the index the
+// two copies sat 16 KB apart, in the same banks: r2f ncu, 8.8e9 bank conflicts
+// and MIO throttle 7.1 per issue).  PGD_TAB32: 4-byte entries (M's hi word; its
+// lo word is 0) -- half the shared-memory wavefronts per lookup.
+#ifndef PGD_TAB32
+#define PGD_TAB32 1
+#endif
+constexpr int DT_SIZE = 2048;
 
 // M(E) for the binade of a binary64 whose hi word >> 20 is i.  Entries outside
 // |E| <= 110 (and zero, i = 0 / 2048) are never used to round a nonzero value
@@ -62,10 +71,35 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
-// table entry of the binade of x (tab0: shared-memory byte address of entry 0)
-__device__ __forceinline__ double mtab(double x, uint32_t tab0) {
-  return lds_f64(tab0 + (((uint32_t)__double2hiint(x) >> 20) << 3));
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
+
+// the table's element type and its fill value for entry i
+#if PGD_TAB32
+using dtab_t = uint32_t;
+__device__ __forceinline__ uint32_t dtab_fill(int i) { return (uint32_t)__double2hiint(dtab_entry(i)); }
+#else
+using dtab_t = double;
+__device__ __forceinline__ double dtab_fill(int i) { return dtab_entry(i); }
+#endif
+
+// table entry for a binary64 hi word h (tab0: shared-memory byte address of entry 0)
+__device__ __forceinline__ double mtab_h(uint32_t h, uint32_t tab0) {
+#if PGD_TAB32
+  // lo word = the entry's byte offset: any lo word with an even last bit keeps
+  // M / q even and M inside its binade, and the offset register is live anyway
+  const uint32_t off = ((h >> 20) & 0x7FFu) << 2;
+  return __hiloint2double((int)lds_u32(tab0 + off), (int)off);
+#else
+  return lds_f64(tab0 + (((h >> 20) & 0x7FFu) << 3));
+#endif
+}
+
+// table entry of the binade of x
+__device__ __forceinline__ double mtab(double x, uint32_t tab0) { return mtab_h((uint32_t)__double2hiint(x), tab0); }
 
 // the odd one of two adjacent binary64 patterns' low words: d's if d is odd, else u's
 // (LOP3 with a predicate output + SEL)
@@ -87,7 +121,7 @@ __device__ __forceinline__ double dmac(double c, double a, double b, uint32_t ta
   // and the hi word of the odd one is the smaller hi word (a carry only leaves an odd p)
   const uint32_t ylo = odd_lo(dlo, ulo);
   const uint32_t yhi = umin(dhi, uhi);
-  const double Mc = lds_f64(tab0 + ((dhi >> 20) << 3));
+  const double Mc = mtab_h(dhi, tab0);
   return __dsub_rn(__dadd_rn(__hiloint2double((int)yhi, (int)ylo), Mc), Mc);   // c (+) P
 }
 
@@ -98,7 +132,7 @@ __device__ __forceinline__ double dadd_pos(double c, double P, uint32_t tab0) {
   const uint32_t ulo = (uint32_t)__double2loint(u), uhi = (uint32_t)__double2hiint(u);
   const uint32_t ylo = odd_lo(dlo, ulo);
   const uint32_t yhi = umin(dhi, uhi);
-  const double Mc = lds_f64(tab0 + ((dhi >> 20) << 3));
+  const double Mc = mtab_h(dhi, tab0);
   return __dsub_rn(__dadd_rn(__hiloint2double((int)yhi, (int)ylo), Mc), Mc);
 }
 

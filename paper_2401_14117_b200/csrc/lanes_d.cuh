@@ -1,0 +1,88 @@
+// lanes_d.cuh -- the binary64-pipe MAC (gemm_d.cuh) for the panel-side
+// kernels: lane values kept as exact binary64 numbers, and the per-binade
+// rounding constant M(E) computed in registers instead of read from a
+// shared-memory table (these kernels are latency-bound, and their shared
+// memory holds their tiles).
+//
+// Contract as lanes.cuh (reading Q6): every update c <- c (-) a (x) b
+// is one rounded product and one rounded difference; values and operands
+// outside the D-MAC's exact range (zero / NaR operands, |E| > 37 operands,
+// |E| > 75 values) take the generic pattern path; both give the same bits.
+#pragma once
+#include <stdint.h>
+#include "posit32.cuh"
+#include "gemm_d.cuh"
+
+namespace pld {
+
+// M(E) = 1.5 * 2^(E - f_s(E) + 52) for the binade of x (hi word h): biased
+// exponent eb + 25 + t(E), E = eb - 1023 (gemm_d.cuh's table, computed).
+// Zero (eb = 0) gets a tiny normal M, which leaves 0 at 0.
+__device__ __forceinline__ double m_of(double x) {
+  const uint32_t h = (uint32_t)__double2hiint(x);
+  const int32_t eb = (int32_t)((h >> 20) & 0x7FFu);
+  const int32_t E = eb - 1023;
+  const int32_t t = (E ^ (E >> 31)) >> 2;
+  return __hiloint2double((int)((((uint32_t)(eb + 25 + t)) << 20) | 0x80000u), 0);
+}
+
+// a (x) b and c (+) p on exact posit values inside the fast range
+__device__ __forceinline__ double mul_r(double a, double b) {
+  const double M = m_of(__dmul_rn(a, b));
+  return __dsub_rn(__fma_rn(a, b, M), M);
+}
+__device__ __forceinline__ double add_r(double c, double p) {
+  const double d = __dadd_rd(c, p), u = __dadd_ru(c, p);
+  const uint32_t dlo = (uint32_t)__double2loint(d), dhi = (uint32_t)__double2hiint(d);
+  const uint32_t ulo = (uint32_t)__double2loint(u), uhi = (uint32_t)__double2hiint(u);
+  const double y = __hiloint2double((int)umin(dhi, uhi), (int)pgd::odd_lo(dlo, ulo));
+  const double M = m_of(d);
+  return __dsub_rn(__dadd_rn(y, M), M);
+}
+
+// |E| of a binary64 value's binade (zero: a large negative number)
+__device__ __forceinline__ int32_t ebin(double x) {
+  return (int32_t)(((uint32_t)__double2hiint(x) >> 20) & 0x7FFu) - 1023;
+}
+
+// a lane value: exact binary64 (dec) or a pattern outside the fast range
+struct LD {
+  double v;
+  uint32_t pat;
+  bool dec;
+};
+
+// value range of a fast lane: 0 or |E| <= 75
+__device__ __forceinline__ bool in_lane_range(double v) {
+  const int32_t e = ebin(v);
+  return e <= 75 && (e >= -75 || e == -1023);
+}
+
+__device__ __forceinline__ void ld_load(LD& c, uint32_t x) {
+  c.pat = x;
+  double v;
+  c.dec = pgd::d_decode(x, v) && in_lane_range(v);
+  c.v = v;
+}
+
+__device__ __forceinline__ uint32_t ld_pattern(const LD& c) { return c.dec ? pgd::d_encode(c.v) : c.pat; }
+
+// operand view: nonzero and |E| <= 37
+__device__ __forceinline__ bool op_fast(double v) {
+  const int32_t e = ebin(v);
+  return e <= 37 && e >= -37;
+}
+
+// c <- c (-) a (x) b: a, b exact values (afast / bfast: inside the operand
+// range), ap / bp their patterns for the generic path
+__device__ __forceinline__ void ld_fms(LD& c, double a, bool afast, uint32_t ap, double b, bool bfast, uint32_t bp) {
+  if (afast && bfast && c.dec) {
+    c.v = add_r(c.v, -mul_r(a, b));
+    c.dec = in_lane_range(c.v);
+    if (!c.dec) c.pat = pgd::d_encode(c.v);
+  } else {
+    ld_load(c, p32::sub(ld_pattern(c), p32::mul(ap, bp)));
+  }
+}
+
+}  // namespace pld
