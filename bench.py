@@ -26,7 +26,7 @@ written by tools/oracle_digests.py): "parity" keys.
 --impl reference        the CPU oracle (oracle/), on this box's host cores, on a
                         bounded sample of the same workload (rank 0 only).
 
-Extra keys: roofline (issue-bound integer ALU roofline of the GEMM kernel,
+Extra keys: roofline (issue-slot roofline of the GEMM kernel and its FP64-pipe use,
 instruction count bound to the kernel's SASS hash), cpu_baseline (oracle
 sample), e2e (posit_gemm_host with pinned host buffers, copies inside the timed
 region), clocks (nvidia-smi during the timed region), gpu_launches (our kernel
@@ -482,11 +482,17 @@ def kernel_sass_sha(kernel_mangled: str):
 
 
 def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):
-    """Issue-bound integer roofline of the GEMM kernel, timed live with CUDA events
-    on the launching stream (copy excluded), against SMs x 128 lanes x clock."""
+    """Issue-slot roofline of the GEMM kernel, timed live with CUDA events on the
+    launching stream (copy excluded), against SMs x 128 lanes x clock (one
+    warp-instruction per SMSP per clock).  Both MACs are bound by issue plus
+    their busiest pipe: the integer MAC by the ALU pipe, the binary64-pipe MAC
+    (the default) by the FP64 pipe, whose use is reported beside the issue
+    fraction (its own measured rate, profiles/pipebench_b200.json)."""
     import torch
     peaks = _load_json(PEAKS_PATH) or {}
-    prof = _load_json(PROFILE_PATH) or {}
+    allp = _load_json(PROFILE_PATH) or {}
+    dpath = os.environ.get("POSIT_GEMM_PATH", "1") != "0"
+    prof = allp.get("d_mac", {}) if dpath else allp
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     times = []
@@ -504,17 +510,26 @@ def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):
     src = f"ncu smsp__inst_executed.sum x 32 / MACs (profiles/gemm_kernel_profile.json, {prof.get('tag')})"
     if inst_per_mac is None:
         inst_per_mac = prof.get("static_inst_per_mac", 54.1)
-        src = "static SASS count of the inner loop (tools/sass_stats.py); no ncu capture yet"
+        src = "static SASS count of the inner loop (tools/sass_loop.py); no ncu capture yet"
     sass = kernel_sass_sha(prof["kernel_mangled"]) if prof.get("kernel_mangled") else None
     peak = n_sm * LANES_PER_SM * f_max / 1e12
     achieved = macs * inst_per_mac / t / 1e12
-    return {"bound": "alu", "unit": "Tinst/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
-            "traffic": prof.get("dram_bytes_per_launch"), "kernel": prof.get("kernel", "pg::k_gemm (NN)"),
-            "kernel_ms": t * 1e3, "inst_per_mac": inst_per_mac, "inst_per_mac_source": src,
-            "sass_sha256": sass, "inst_per_mac_stale": (None if sass is None else sass != prof.get("sass_sha256")),
-            "peak_source": f"{n_sm} SMs x 4 SMSP x 32 lanes x sm_max_mhz {f_max / 1e6:.0f} (MEASURED_PEAKS.json) "
-                           "= warp-instruction issue limit; see DESIGN.md",
-            "posit_tflops_kernel": 2 * macs / t / 1e12}
+    out = {"bound": "alu", "unit": "Tinst/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+           "traffic": prof.get("dram_bytes_per_launch"), "kernel": prof.get("kernel", "pg::k_gemm (NN)"),
+           "kernel_ms": t * 1e3, "inst_per_mac": inst_per_mac, "inst_per_mac_source": src,
+           "sass_sha256": sass, "inst_per_mac_stale": (None if sass is None else sass != prof.get("sass_sha256")),
+           "peak_source": f"{n_sm} SMs x 4 SMSP x 32 lanes x sm_max_mhz {f_max / 1e6:.0f} (MEASURED_PEAKS.json) "
+                          "= warp-instruction issue limit; see DESIGN.md",
+           "posit_tflops_kernel": 2 * macs / t / 1e12,
+           "mac": "binary64 pipe (D-MAC)" if dpath else "integer pipes"}
+    if dpath and prof.get("fp64_cycles_per_mac"):
+        # binary64 pipe: its busy cycles per warp-MAC (DADD / DMUL 1 / 1.83, DFMA 1 / 1.47 SM-clocks,
+        # measured) against the clock
+        busy = macs / 32.0 * prof["fp64_cycles_per_mac"] / n_sm / (t * f_max)
+        out["fp64_pipe"] = {"frac": busy, "fp64_inst_per_mac": prof.get("fp64_inst_per_mac"),
+                            "cycles_per_warp_mac": prof["fp64_cycles_per_mac"],
+                            "source": "profiles/pipebench_b200.json rates x the kernel's FP64 instruction mix"}
+    return out
 
 
 def main():

@@ -13,6 +13,14 @@ static std::atomic<unsigned long long> g_launches{0};
 
 void pb_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pb_dpath() {
+  static const bool v = [] {
+    const char* e = getenv("POSIT_GEMM_PATH");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 int pb_device() {
   int d = 0;
   if (cudaGetDevice(&d) != cudaSuccess || d < 0) { (void)cudaGetLastError(); d = 0; }

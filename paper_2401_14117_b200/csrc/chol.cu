@@ -1,6 +1,7 @@
 // chol.cu -- the diagonal-block Cholesky (potf2) and the
 // tiny one-thread-per-output GEMM / SYRK it and the LU panel use.
 #include "lanes.cuh"
+#include "lanes_d.cuh"
 
 namespace pl {
 
@@ -294,10 +295,43 @@ __global__ void __launch_bounds__(256) k_gemm_tiny(pg::Params P, int transb, int
   P.C[i * P.ldc + j] = lv_pattern(c);
 }
 
+// The same with binary64 lane values (lanes_d.cuh: the D-MAC, constants in registers)
+__global__ void __launch_bounds__(256) k_gemm_tiny_d(pg::Params P, int transb, int syrk) {
+  if (P.stop != nullptr && *P.stop != 0) return;
+  const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
+  if (i >= P.m || j >= P.n || (syrk && j > i)) return;
+  pld::LD c;
+  pld::ld_load(c, P.beta ? P.C[i * P.ldc + j] : 0u);
+  constexpr int CH = 8;
+  const int64_t sa = P.transa ? P.lda : 1, sa0 = P.transa ? i : i * P.lda;
+  const int64_t sb = transb ? 1 : P.ldb, sb0 = transb ? j * P.ldb : j;
+  for (int64_t q0 = 0; q0 < P.k; q0 += CH) {
+    uint32_t a[CH], b[CH];
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const bool in = q0 + u < P.k;
+      a[u] = in ? P.A[sa0 + (q0 + u) * sa] : 0u;
+      b[u] = in ? P.B[sb0 + (q0 + u) * sb] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      if (q0 + u < P.k) {
+        const uint32_t bp = P.neg ? b[u] : 0u - b[u];   // c (+) a b = c (-) a (-b), negation exact
+        uint32_t sa_ = 0u, sb_ = 0u;
+        const double ad = pgd::stage_decode_d(a[u], 0u, sa_), bd = pgd::stage_decode_d(bp, 0u, sb_);
+        pld::ld_fms(c, ad, sa_ == 0u, a[u], bd, sb_ == 0u, bp);
+      }
+    }
+  }
+  P.C[i * P.ldc + j] = pld::ld_pattern(c);
+}
+
 int pb_launch_gemm_tiny(const pg::Params& P, bool transb, bool syrk, cudaStream_t st) {
   pb_count_launch();
   const dim3 grid((unsigned)((P.n + 15) / 16), (unsigned)((P.m + 15) / 16));
-  k_gemm_tiny<<<grid, 256, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
+  if (pb_dpath()) k_gemm_tiny_d<<<grid, 256, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
+  else k_gemm_tiny<<<grid, 256, 0, st>>>(P, transb ? 1 : 0, syrk ? 1 : 0);
   return last_launch();
 }
 
@@ -323,6 +357,23 @@ __global__ void __launch_bounds__(256) k_syrk_tiny(int64_t n, int64_t k, const u
     lv_fms(c, ap, af, ad, bv.a.M, bv.a.E, bv.a.sg, lv_operand(bv), bp);
   }
   C[i * ldc + j] = lv_pattern(c);
+}
+
+__global__ void __launch_bounds__(256) k_syrk_tiny_d(int64_t n, int64_t k, const uint32_t* A, int64_t lda, uint32_t* C,
+                                                     int64_t ldc, const int32_t* stop) {
+  if (stop != nullptr && *stop != 0) return;
+  const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
+  if ((int64_t)blockIdx.x > (int64_t)blockIdx.y || i >= n || j > i) return;
+  pld::LD c;
+  pld::ld_load(c, C[i * ldc + j]);
+  for (int64_t q = 0; q < k; q++) {
+    const uint32_t ap = A[i * lda + q], bp = A[j * lda + q];
+    uint32_t sa_ = 0u, sb_ = 0u;
+    const double ad = pgd::stage_decode_d(ap, 0u, sa_), bd = pgd::stage_decode_d(bp, 0u, sb_);
+    pld::ld_fms(c, ad, sa_ == 0u, ap, bd, sb_ == 0u, bp);
+  }
+  C[i * ldc + j] = pld::ld_pattern(c);
 }
 
 // Diagonal-block Cholesky: one cluster launch for 32 < b <= 256
@@ -379,7 +430,8 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
         if ((rc = pb_trsm_rltn(r, jb, Ajj, lda, Ajj + jb * lda, lda, info, st))) return rc;
         pb_count_launch();
         const unsigned t = (unsigned)((r + 15) / 16);
-        k_syrk_tiny<<<dim3(t, t), 256, 0, st>>>(r, jb, Ajj + jb * lda, lda, Ajj + jb * lda + jb, lda, info);
+        if (pb_dpath()) k_syrk_tiny_d<<<dim3(t, t), 256, 0, st>>>(r, jb, Ajj + jb * lda, lda, Ajj + jb * lda + jb, lda, info);
+        else k_syrk_tiny<<<dim3(t, t), 256, 0, st>>>(r, jb, Ajj + jb * lda, lda, Ajj + jb * lda + jb, lda, info);
       }
     }
     return last_launch();

@@ -496,11 +496,7 @@ int pb_launch_gemm(const pg::Params& P, bool transb, bool syrk, cudaStream_t st,
   if (tiny_env == 2 && P.k >= 1 && P.k <= 32 && P.n <= 32 && !syrk) return pb_launch_gemm_tiny(P, transb, syrk, st);
   int v = variant();
   // the binary64-pipe MAC (gemm_d.cu) unless POSIT_GEMM_PATH=0 or an integer-MAC tile is forced (11..14)
-  static const int path_env = [] {
-    const char* e = getenv("POSIT_GEMM_PATH");
-    return e ? atoi(e) : 1;
-  }();
-  if ((path_env != 0 && (v == 0 || v >= 21)) || v >= 21) return pb_launch_gemm_d(P, transb, syrk, st, pdl, v);
+  if ((pb_dpath() && v == 0) || v >= 21) return pb_launch_gemm_d(P, transb, syrk, st, pdl, v);
   if (v == 0) {
     // the smallest modelled time; near-ties (within 10%) go to the first candidate
     auto pick = [&](int v0, double w0, std::initializer_list<std::pair<int, double>> rest) {

@@ -101,18 +101,32 @@ __device__ __forceinline__ double mtab_h(uint32_t h, uint32_t tab0) {
 // table entry of the binade of x
 __device__ __forceinline__ double mtab(double x, uint32_t tab0) { return mtab_h((uint32_t)__double2hiint(x), tab0); }
 
+// M(E) computed in registers: biased exponent eb + 25 + t(E), E = eb - 1023
+// (zero, eb = 0, gets a tiny normal M, which leaves 0 at 0)
+__device__ __forceinline__ double m_reg(double x) {
+  const uint32_t h = (uint32_t)__double2hiint(x);
+  const int32_t eb = (int32_t)((h >> 20) & 0x7FFu);
+  const int32_t E = eb - 1023;
+  const int32_t t = (E ^ (E >> 31)) >> 2;
+  return __hiloint2double((int)((((uint32_t)(eb + 25 + t)) << 20) | 0x80000u), 0);
+}
+
+#ifndef PGD_PROD_REG                 // 1: the product's M from registers (one table lookup per MAC instead of two)
+#define PGD_PROD_REG 0
+#endif
+
 // the odd one of two adjacent binary64 patterns' low words: d's if d is odd, else u's
-// (LOP3 with a predicate output + SEL)
+// (LOP3 a & b, LUT 0xC0, with a predicate output + SEL)
 __device__ __forceinline__ uint32_t odd_lo(uint32_t dlo, uint32_t ulo) {
   uint32_t y, t;
-  asm("{\n\t.reg .pred p;\n\tlop3.or.b32 %1|p, %2, 1, 0, 0x80, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+  asm("{\n\t.reg .pred p;\n\tlop3.or.b32 %1|p, %2, 1, 0, 0xC0, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
       : "=r"(y), "=r"(t) : "r"(dlo), "r"(ulo));
   return y;
 }
 
 // c (+) (a (x) b): a, b, c exact posit values in binary64, inside the fast range
 __device__ __forceinline__ double dmac(double c, double a, double b, uint32_t tab0) {
-  const double Mp = mtab(__dmul_rn(a, b), tab0);
+  const double Mp = PGD_PROD_REG ? m_reg(__dmul_rn(a, b)) : mtab(__dmul_rn(a, b), tab0);
   const double P = __dsub_rn(__fma_rn(a, b, Mp), Mp);     // a (x) b
   const double d = __dadd_rd(c, P), u = __dadd_ru(c, P);
   const uint32_t dlo = (uint32_t)__double2loint(d), dhi = (uint32_t)__double2hiint(d);

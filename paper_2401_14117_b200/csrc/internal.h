@@ -39,6 +39,10 @@ int pb_from_f64(const double* x, uint32_t* out, int64_t count, cudaStream_t st);
 int pb_to_f64(const uint32_t* p, double* out, int64_t count, cudaStream_t st);
 int pb_gemm_guarded(const pg::Params& P, bool transb, bool syrk, const int32_t* stop_flag, cudaStream_t st);
 
+// POSIT_GEMM_PATH: 1 (default) = the binary64-pipe MAC (gemm_d.cuh, lanes_d.cuh)
+// in every kernel that has it, 0 = the integer MAC everywhere (same bits)
+bool pb_dpath();
+
 // number of kernels this library has launched (posit_kernel_launches)
 void pb_count_launch();
 

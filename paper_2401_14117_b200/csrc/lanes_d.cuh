@@ -15,16 +15,8 @@
 
 namespace pld {
 
-// M(E) = 1.5 * 2^(E - f_s(E) + 52) for the binade of x (hi word h): biased
-// exponent eb + 25 + t(E), E = eb - 1023 (gemm_d.cuh's table, computed).
-// Zero (eb = 0) gets a tiny normal M, which leaves 0 at 0.
-__device__ __forceinline__ double m_of(double x) {
-  const uint32_t h = (uint32_t)__double2hiint(x);
-  const int32_t eb = (int32_t)((h >> 20) & 0x7FFu);
-  const int32_t E = eb - 1023;
-  const int32_t t = (E ^ (E >> 31)) >> 2;
-  return __hiloint2double((int)((((uint32_t)(eb + 25 + t)) << 20) | 0x80000u), 0);
-}
+// M(E) in registers (gemm_d.cuh's table, computed)
+__device__ __forceinline__ double m_of(double x) { return pgd::m_reg(x); }
 
 // a (x) b and c (+) p on exact posit values inside the fast range
 __device__ __forceinline__ double mul_r(double a, double b) {

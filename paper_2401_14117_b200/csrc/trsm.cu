@@ -2,6 +2,8 @@
 // L11^-1 A12 (left, lower, unit) and L21 = A21 L11^-T (right, lower,
 // transposed, non-unit).
 #include "lanes.cuh"
+#include "lanes_d.cuh"
+#include <type_traits>
 
 namespace pl {
 
@@ -298,12 +300,17 @@ constexpr int FR_NMAX = 256;
 // chunks of CH columns; CH < FR_NMAX halves the shared memory (with the
 // in-block MAC's product table computed in registers instead of read from
 // shared memory) so that three CTAs fit an SM.
-template <int W, int FR_ROWS, int CH = FR_NMAX>
+// DM: the update loop on the binary64-pipe MAC (gemm_d.cuh): L and the block's
+// values staged as exact binary64 numbers (8 bytes instead of 16), the D-MAC's
+// 8 KB table instead of the PIX table, and the in-block MAC's product table in
+// registers -- 72 KB, three CTAs per SM.
+template <int W, int FR_ROWS, int CH = FR_NMAX, bool DM = false>
 struct FrSmem {
-  static constexpr bool TP = CH == FR_NMAX;   // the in-block MAC's product table in shared memory
+  static constexpr bool TP = CH == FR_NMAX && !DM;   // the in-block MAC's product table in shared memory
+  using LT = std::conditional_t<DM, double, uint4>;
   uint32_t b[FR_ROWS][FR_NMAX + 1];          // the CTA's rows of B (patterns)
-  uint4 ld[W][CH];                            // L[j][c0 + k] decoded A-format {M, E, sigma (0: slow), pattern}
-  uint4 bop[FR_ROWS][W];                      // block J's final values, B-format {M, E, sg (0: slow), pattern}
+  LT ld[W][CH];                               // L[j][c0 + k] decoded: A-format {M, E, sigma, .w} or binary64
+  LT bop[FR_ROWS][W];                         // block J's final values (negated), B-format or binary64
   uint32_t lblk[W][W + 1];                    // L's diagonal block J (patterns)
   uint4 lblkd[W][W];                          // the same, decoded A-format {M, E, sigma, fast}
   uint4 ldiag[W];                             // L[c0 + k][c0 + k] as a divisor {M hidden@30, E, sg, fast}
@@ -313,16 +320,17 @@ struct FrSmem {
   uint4 tp[TP ? pg::TSIZE : 1];              // the MAC's per-scale constant tables
   uint4 tx[pg::TSIZE];
 #if PG_RLTN_PIX
-  uint4 tpx[pg::PIX_NE];                      // the PIX product table of the update loop
+  uint4 tpx[DM ? 1 : pg::PIX_NE];             // the PIX product table of the update loop
 #endif
+  pgd::dtab_t dtab[DM ? pgd::DT_SIZE : 1];    // the D-MAC's table
 };
 
-template <int W, int FR_ROWS, int CH = FR_NMAX, int MINB = 2>
+template <int W, int FR_ROWS, int CH = FR_NMAX, int MINB = 2, bool DM = false>
 __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uint32_t* L, int64_t ldl, uint32_t* B,
                                                                     int64_t ldb, int64_t m, int64_t n,
                                                                     const int32_t* stop, int one) {
   constexpr int NT = FR_ROWS * W;
-  using Sm = FrSmem<W, FR_ROWS, CH>;
+  using Sm = FrSmem<W, FR_ROWS, CH, DM>;
   extern __shared__ __align__(16) unsigned char fr_raw[];
   Sm& S = *reinterpret_cast<Sm*>(fr_raw);
   if (stop != nullptr && *stop != 0) return;
@@ -337,9 +345,12 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
   K.tp0 = (uint32_t)__cvta_generic_to_shared(S.tp + (Sm::TP ? pg::TBIAS : 0));
   K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
 #if PG_RLTN_PIX
-  pg::fill_prod_pix<false>(S.tpx, tid, NT);
+  if constexpr (!DM) pg::fill_prod_pix<false>(S.tpx, tid, NT);
   const uint32_t tpx0 = (uint32_t)__cvta_generic_to_shared(S.tpx + 2 * pg::PIX_SB);
 #endif
+  if constexpr (DM)
+    for (int i = tid; i < pgd::DT_SIZE; i += NT) S.dtab[i] = pgd::dtab_fill(i);
+  const uint32_t dtab0 = (uint32_t)__cvta_generic_to_shared(S.dtab);
   for (int e = tid; e < FR_ROWS * (int)n; e += NT) {
     const int rr = e / (int)n, cc = e % (int)n;
     S.b[rr][cc] = rr < rows ? B[(r0 + rr) * ldb + cc] : 0u;
@@ -379,18 +390,30 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
         for (int k = 0; k < W; k++) xs[k] = L[(int64_t)j * ldl + c0 + k];
 #pragma unroll
         for (int k = 0; k < W; k++) {
-          uint4 d;
-          const bool fk = fast_a(xs[k], d);
-          S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(xs[k], d.y));
-          f &= (int)fk;
+          if constexpr (DM) {
+            uint32_t sp = 0u;
+            S.ld[k][jj] = pgd::stage_decode_d(xs[k], 0u, sp);
+            f &= (int)(sp == 0u);
+          } else {
+            uint4 d;
+            const bool fk = fast_a(xs[k], d);
+            S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(xs[k], d.y));
+            f &= (int)fk;
+          }
         }
       } else {
         for (int k = 0; k < jb; k++) {
           const uint32_t x = L[(int64_t)j * ldl + c0 + k];
-          uint4 d;
-          const bool fk = fast_a(x, d);
-          S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(x, d.y));
-          f &= (int)fk;
+          if constexpr (DM) {
+            uint32_t sp = 0u;
+            S.ld[k][jj] = pgd::stage_decode_d(x, 0u, sp);
+            f &= (int)(sp == 0u);
+          } else {
+            uint4 d;
+            const bool fk = fast_a(x, d);
+            S.ld[k][jj] = make_uint4(d.x, d.y, d.z, FR_LW(x, d.y));
+            f &= (int)fk;
+          }
         }
       }
       S.colfast[j] = f;
@@ -443,7 +466,13 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
         const uint32_t x = lv_pattern(v);
         S.b[r][c0 + c] = x;
         // sign pre-negated: c (-) a b
-        S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), FR_BW(x, (uint32_t)v.a.E));
+        if constexpr (DM) {
+          double vd;
+          pgd::d_decode(x, vd);                             // exact (used only when the row's values are fast)
+          S.bop[r][c] = -vd;
+        } else {
+          S.bop[r][c] = make_uint4(v.a.M, (uint32_t)v.a.E, (uint32_t)(-v.a.sg), FR_BW(x, (uint32_t)v.a.E));
+        }
       }
       if (c == 0) S.rowfast[r] = allf ? 1 : 0;
     }
@@ -465,6 +494,40 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
       const bool rf = S.rowfast[r] != 0;
       constexpr int G = 4;
       for (int col0 = ch0 + c; col0 < chend; col0 += G * W) {
+        if constexpr (DM) {
+          double a[G];
+          uint32_t x[G];
+          bool ok = rf;
+#pragma unroll
+          for (int u = 0; u < G; u++) {
+            const int col = col0 + u * W;
+            const bool in = col < chend;
+            x[u] = in ? S.b[r][col] : 0u;
+            const bool d = pgd::d_decode(x[u], a[u]) && pld::in_lane_range(a[u]);
+            ok = ok && d && (!in || S.colfast[col] != 0);
+          }
+          if (ok) {
+#pragma unroll 2
+            for (int k = 0; k < jb; k++) {
+              const double bd = S.bop[r][k];
+#pragma unroll
+              for (int u = 0; u < G; u++) a[u] = pgd::dmac(a[u], S.ld[k][min(col0 + u * W, chend - 1) - ch0], bd, dtab0);
+            }
+#pragma unroll
+            for (int u = 0; u < G; u++)
+              if (col0 + u * W < chend) S.b[r][col0 + u * W] = pgd::d_encode(a[u]);
+            continue;
+          }
+#pragma unroll 1
+          for (int u = 0; u < G; u++) {
+            const int col = col0 + u * W;
+            if (col >= chend) break;
+            uint32_t y = x[u];
+            for (int k = 0; k < jb; k++) y = sub(y, mul(L[(int64_t)col * ldl + c0 + k], S.b[r][c0 + k]));
+            S.b[r][col] = y;
+          }
+          continue;
+        } else {
         pg::Acc a[G];
         uint32_t x[G];
         bool ok = rf;
@@ -504,6 +567,7 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
             for (int k = 0; k < jb; k++) y = sub(y, mul(FR_LPAT(col, k), S.b[r][c0 + k]));
             S.b[r][col] = y;
           }
+        }
         }
       }
     }
@@ -584,12 +648,17 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
                            (int)sizeof(FrSmem<8, 16>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<8, 32>));
+      cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16, FR_NMAX, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(FrSmem<16, 16, FR_NMAX, true>));
     });
     pb_count_launch();
 #define PB_RLTN(W_, R_, ...)                                                                                         \
   k_trsm_rltn_fused<W_, R_, ##__VA_ARGS__><<<(unsigned)((m + R_ - 1) / R_), R_ * W_,                              \
                                               sizeof(FrSmem<W_, R_, ##__VA_ARGS__>), st>>>(L, ldl, B, ldb, m, n, stop, 1)
-    if (var == 1632) PB_RLTN(16, 32);
+    if (pb_dpath() && var == 1616)
+      k_trsm_rltn_fused<16, 16, FR_NMAX, 3, true><<<(unsigned)((m + 15) / 16), 256, sizeof(FrSmem<16, 16, FR_NMAX, true>),
+                                                    st>>>(L, ldl, B, ldb, m, n, stop, 1);
+    else if (var == 1632) PB_RLTN(16, 32);
     else if (var == 816) PB_RLTN(8, 16);
     else if (var == 832) PB_RLTN(8, 32);
     else if (var == 101616) k_trsm_rltn_fused<16, 16, 128, 3><<<(unsigned)((m + 15) / 16), 256,
