@@ -4,6 +4,7 @@
 // recursive getrf2 traversal around it; the fused tail factors a whole
 // trailing block the same way.
 #include "lanes.cuh"
+#include "lanes_d.cuh"
 
 namespace pl {
 
@@ -241,7 +242,9 @@ __device__ __forceinline__ void leaf_publish(const uint32_t* tile, int W, int64_
     for (int c = tid; c < W; c += NT) jrow[par * WMAX + c] = tile[(int)(jn - rb) * W + c];
 }
 
-template <int WMAX>
+// DM: the in-panel update on the binary64-pipe MAC (gemm_d.cuh), the pivot row
+// staged as exact binary64 numbers (negated) with a fast flag
+template <int WMAX, bool DM = false>
 __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, int64_t m, int64_t w,
                                                      int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
                                                      int64_t row_base, LeafWs* ws, uint32_t* cand, uint32_t* jrow) {
@@ -249,13 +252,19 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long cbest;                // this CTA's best candidate key (next column)
   __shared__ uint32_t srow[2 * WMAX];                 // the published rows p and j of the current column
-  __shared__ uint4 urow[WMAX];                        // the pivot row as decoded B operands {M, E, sg, fast}
+  __shared__ uint4 urow[DM ? 1 : WMAX];               // the pivot row as decoded B operands {M, E, sg, fast}
   __shared__ uint32_t urowp[WMAX];                    // ... and as patterns
+  __shared__ double urowd[DM ? WMAX : 1];             // DM: -(pivot row) in binary64
+  __shared__ uint8_t urowf[DM ? WMAX : 1];            // DM: fast-operand flags
+  __shared__ pgd::dtab_t dtab[DM ? pgd::DT_SIZE : 1];
   __shared__ uint4 tp[pg::TSIZE], tx[pg::TSIZE];      // the MAC's constant tables
   const int NT = blockDim.x;
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
   pg::fill_tables(tp, tx, tid, NT);
+  if constexpr (DM)
+    for (int i = tid; i < pgd::DT_SIZE; i += NT) dtab[i] = pgd::dtab_fill(i);
+  const uint32_t dtab0 = (uint32_t)__cvta_generic_to_shared(dtab);
   pg::MacConst K;
   K.one = 1u;
   K.sixteen = 16u;
@@ -306,10 +315,16 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
     }
     const int usrc = swp ? 0 : W;                     // the row now at position j
     for (int c = tid; c < W; c += NT) {
-      LaneVal t;
       const uint32_t x = srow[usrc + c];
-      lv_load(t, x);
-      urow[c] = make_uint4(t.a.M, (uint32_t)t.a.E, (uint32_t)t.a.sg, lv_operand(t) ? 1u : 0u);
+      if constexpr (DM) {
+        uint32_t sp = 0u;
+        urowd[c] = pgd::stage_decode_d(x, 1u, sp);     // negated: c (-) l u = c (+) l (-u)
+        urowf[c] = sp == 0u ? 1 : 0;
+      } else {
+        LaneVal t;
+        lv_load(t, x);
+        urow[c] = make_uint4(t.a.M, (uint32_t)t.a.E, (uint32_t)t.a.sg, lv_operand(t) ? 1u : 0u);
+      }
       urowp[c] = x;
     }
     __syncthreads();
@@ -337,13 +352,24 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
         const int i = i0 + (int)ii;
         const int q = (int)j + 1 + (int)(e - ii * (uint32_t)wq);
         const uint32_t lp = tile[i * W + (int)j];
-        uint4 ad;
-        const bool af = fast_a(lp, ad);
-        const uint4 ub = urow[q];
-        LaneVal c;
-        lv_load(c, tile[i * W + q]);
-        lv_fms_t(c, lp, af, ad, ub.x, (int32_t)ub.y, (int32_t)ub.z, ub.w != 0u, urowp[q], K);
-        const uint32_t nv = lv_pattern(c);
+        uint32_t nv;
+        if constexpr (DM) {
+          uint32_t sp = 0u;
+          const double l = pgd::stage_decode_d(lp, 0u, sp);
+          const uint32_t cx = tile[i * W + q];
+          double cv;
+          const bool cd = pgd::d_decode(cx, cv) && pld::in_lane_range(cv);
+          nv = (sp == 0u && urowf[q] != 0 && cd) ? pgd::d_encode(pgd::dmac(cv, l, urowd[q], dtab0))
+                                                 : sub(cx, mul(lp, urowp[q]));
+        } else {
+          uint4 ad;
+          const bool af = fast_a(lp, ad);
+          const uint4 ub = urow[q];
+          LaneVal c;
+          lv_load(c, tile[i * W + q]);
+          lv_fms_t(c, lp, af, ad, ub.x, (int32_t)ub.y, (int32_t)ub.z, ub.w != 0u, urowp[q], K);
+          nv = lv_pattern(c);
+        }
         tile[i * W + q] = nv;
         if (q == (int)j + 1) {
           const unsigned long long k = piv_key(nv, rb + i);
@@ -393,6 +419,8 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     cudaFuncSetAttribute(k_leaf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(k_leaf_coop1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(k_leaf_coop1<TAIL_WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_leaf_coop1<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_leaf_coop1<TAIL_WMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   });
   const int coop = pb_coop_supported() ? coop_env : 0, nsm = pb_num_sms();
   // on the caller's stream: one CTA of 256 threads per SM; on a side stream
@@ -427,7 +455,8 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known; w <= 64)
     const void* kfn = nullptr;
     if (grid <= (unsigned)LEAF_MAXCTA && (coop != 2 || wide_w))
-      kfn = wide_w ? (const void*)k_leaf_coop1<TAIL_WMAX> : (const void*)k_leaf_coop1<64>;
+      kfn = pb_dpath() ? (wide_w ? (const void*)k_leaf_coop1<TAIL_WMAX, true> : (const void*)k_leaf_coop1<64, true>)
+                       : (wide_w ? (const void*)k_leaf_coop1<TAIL_WMAX> : (const void*)k_leaf_coop1<64>);
     else if (!wide_w)
       kfn = (const void*)k_leaf_coop;
     if (kfn != nullptr) {
