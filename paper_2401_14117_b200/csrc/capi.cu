@@ -183,8 +183,13 @@ static int gemm_host_pipelined(char transb, int64_t m, int64_t n, int64_t k, uin
                                int64_t lda, const uint32_t* B, int64_t ldb, uint32_t beta, uint32_t* C, int64_t ldc,
                                uint32_t* dA, uint32_t* dB, uint32_t* dC, cudaStream_t st) {
   const int64_t brow = transb == 'N' ? k : n, bcol = transb == 'N' ? n : k;
-  int64_t nch = m / HOST_CHUNK_MIN;
+  static const int64_t nch_env = [] {          // POSIT_HOST_CHUNKS: row chunks (A/B runs; default m / 512, <= 8)
+    const char* e = getenv("POSIT_HOST_CHUNKS");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  int64_t nch = nch_env > 0 ? nch_env : m / HOST_CHUNK_MIN;
   if (nch > 8) nch = 8;
+  if (nch < 1) nch = 1;
   const int64_t rows = (((m + nch - 1) / nch) + 63) / 64 * 64;
   nch = (m + rows - 1) / rows;
   constexpr int MAXCH = 8;
