@@ -227,6 +227,77 @@ __global__ void __launch_bounds__(LC_T) k_trsm_llnu_col(const uint32_t* L, int64
   }
 }
 
+// ---- unit lower in-block solve on the binary64-pipe MAC: 8 lanes per column ----
+// B[i0 .. i0 + ib) <- L11^-1 B for one 32-row block (unit diagonal), every
+// column of B independent.  Eight lanes share a column, lane t owning rows
+// t, t + 8, t + 16, t + 24: at step k the owner of row k (final: all its
+// updates from rows < k are in) broadcasts it within the 8-lane group and
+// every lane applies b_r <- b_r (-) l_rk (x) b_k to its rows r > k -- the
+// textbook order per element (Q6), 31 short steps with four independent
+// chains per lane, and 8x the threads of the thread-per-column kernel (whose
+// 496-MAC serial chain per thread ran at ~3 warps per SM).
+constexpr int G8_COLS = 32;                   // columns per CTA (256 threads)
+__global__ void __launch_bounds__(256) k_trsm_llnu_g8(const uint32_t* L, int64_t ldl, uint32_t* B, int64_t ldb,
+                                                      int64_t i0, int64_t ib, int64_t n) {
+  __shared__ double sld[TB][TB + 1];          // L[i0 + r][i0 + c] in binary64, r > c
+  __shared__ uint32_t slp[TB][TB + 1];        // the patterns
+  __shared__ uint32_t slf[TB];                // bit c of row r: L[r][c] is a fast operand
+  const int tid = threadIdx.x;
+  const int t = tid & 7;                      // lane in the column group
+  const int64_t col = (int64_t)blockIdx.x * G8_COLS + (tid >> 3);
+  const bool live = col < n;
+  if (tid < TB) slf[tid] = 0u;
+  __syncthreads();
+  for (int e = tid; e < TB * TB; e += 256) {
+    const int r = e / TB, c = e % TB;
+    if (r < ib && c < r) {
+      const uint32_t x = L[(i0 + r) * ldl + i0 + c];
+      uint32_t sp = 0u;
+      sld[r][c] = pgd::stage_decode_d(x, 0u, sp);
+      slp[r][c] = x;
+      if (sp == 0u) atomicOr(&slf[r], 1u << c);
+    }
+  }
+  __syncthreads();
+  pld::LD v[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    const int r = t + 8 * u;
+    pld::ld_load(v[u], (live && r < ib) ? B[(i0 + r) * ldb + col] : 0u);
+  }
+  for (int k = 0; k + 1 < ib; k++) {
+    const int own = k & 7, uk = k >> 3;
+    // the owner's final value of row k
+    double bv = 0.0;
+    uint32_t bp = 0u;
+    bool bdec = false;
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (u == uk) { bv = v[u].v; bp = v[u].pat; bdec = v[u].dec; }
+    if (t == own && bdec) bp = pgd::d_encode(bv);
+    const int src = (tid & 31 & ~7) | own;
+    bv = __shfl_sync(0xFFFFFFFFu, bv, src);
+    bp = __shfl_sync(0xFFFFFFFFu, bp, src);
+    bdec = __shfl_sync(0xFFFFFFFFu, (int)bdec, src) != 0;
+    const bool bfast = bdec && pld::op_fast(bv);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int r = t + 8 * u;
+      if (r > k && r < ib) {
+        const bool af = (slf[r] >> k) & 1u;
+        pld::ld_fms(v[u], sld[r][k], af, slp[r][k], bv, bfast, bp);
+      }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int r = t + 8 * u;
+      if (r < ib) B[(i0 + r) * ldb + col] = pld::ld_pattern(v[u]);
+    }
+  }
+}
+
 // Right, lower, transposed, non-unit: columns j0..j0+jb-1 of B (jb <= 16).
 // Half-warp per row of B (two rows per warp), lane = column (coalesced):
 // step k finalises b_k <- b_k (/) l_kk, broadcasts it within the half-warp,
@@ -599,11 +670,18 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
     const char* e = getenv("POSIT_LLNU_BLK");
     return e ? atoi(e) : 8;
   }();
+  static const int g8_env = [] {                  // POSIT_LLNU_G8=0: the integer-MAC in-block kernels
+    const char* e = getenv("POSIT_LLNU_G8");
+    return e ? atoi(e) : 1;
+  }();
+  const bool g8 = pb_dpath() && g8_env != 0;
   for (int64_t i0 = 0; i0 < m; i0 += TB) {
     const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
     if (ib > 1) {
       pb_count_launch();
-      if (use_col == 8)
+      if (g8)
+        k_trsm_llnu_g8<<<(unsigned)((n + G8_COLS - 1) / G8_COLS), 256, 0, st>>>(L, ldl, B, ldb, i0, ib, n);
+      else if (use_col == 8)
         k_trsm_llnu_col<8><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
       else if (use_col == 4)
         k_trsm_llnu_col<4><<<(unsigned)((n + LC_T - 1) / LC_T), LC_T, 0, st>>>(L, ldl, B, ldb, i0, ib, n, 1);
