@@ -251,6 +251,137 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
   cl.sync();                                                    // no CTA exits while others may still read it
 }
 
+// The same cluster potf2 with binary64 lane values (lanes_d.cuh): each element
+// kept as its exact binary64 value while in the fast range, the column buffer
+// holding {binary64 value, fast flag, pattern} (8 + 1 + 4 bytes pushed per
+// element instead of 36), the updates on the D-MAC.  The division by l_kk and
+// the sqrt stay the integer-path operations (one per element / column).
+struct PcSmemD {
+  uint32_t colp[2][PC_B];                      // column k: patterns l_jk (rows j > k)
+  double cold[2][PC_B];                        // ... as binary64
+  uint8_t colf[2][PC_B];                       // ... fast-operand flags
+  int fail;
+  int lkk_step;
+  uint32_t lkk;
+  uint4 tx[pg::TSIZE];                         // the division's rounding table (integer path)
+};
+
+__device__ __forceinline__ void pcd_fms(pld::LD& x, const PcSmemD& S, int q, int i, int j) {
+  pld::ld_fms(x, S.cold[q][i], S.colf[q][i] != 0, S.colp[q][i], S.cold[q][j], S.colf[q][j] != 0, S.colp[q][j]);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(32 * (PC_B / NC), 1)
+    k_potf2_cluster_d(uint32_t* A, int64_t lda, int b, int32_t* info, int64_t row_base) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = 32 * (PC_B / NC);
+  __shared__ PcSmemD S;
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int i = w * NC + c;
+  if (*info != 0) return;
+  pg::fill_tables<false, false>(S.tx, S.tx, tid, NT);
+  pg::MacConst K;
+  K.one = 1u; K.sixteen = 16u;
+  K.tp0 = 0u;
+  K.tx0 = (uint32_t)__cvta_generic_to_shared(S.tx + pg::TBIAS) - 30u * 16u;
+  if (tid == 0) { S.fail = 0; S.lkk_step = -1; }
+  pld::LD v[PC_Q];
+#pragma unroll
+  for (int q = 0; q < PC_Q; q++) {
+    const int j = l + 32 * q;
+    pld::ld_load(v[q], (i < b && j <= i) ? A[(int64_t)i * lda + j] : 0u);
+  }
+  pld::LD dd;
+  pld::ld_load(dd, tid < b ? A[(int64_t)tid * lda + tid] : 0u);
+  __syncthreads();
+  cl.sync();
+  volatile int* vstep = &S.lkk_step;
+  bool failed = false;
+  for (int k = 0; k < b; k++) {
+    const int qk = k & 1, qp = qk ^ 1;
+    if (k > 0) {
+      pc_wait();
+      if (S.fail) { failed = true; break; }
+    }
+    if (tid < b && tid >= k) {
+      if (k > 0) pcd_fms(dd, S, qp, tid, tid);
+      if (tid == k) {
+        const uint32_t dk = pld::ld_pattern(dd);
+        if ((int32_t)dk <= 0) {
+          S.fail = 1;
+          if (c == 0) *info = (int32_t)(row_base + k + 1);
+        } else {
+          S.lkk = p32::sqrt(dk);
+        }
+        __threadfence_block();
+        *vstep = k;
+      }
+    }
+    if (k > 0 && i < b) {
+#pragma unroll
+      for (int q = 0; q < PC_Q; q++) {
+        const int j = l + 32 * q;
+        if (j >= k && j <= i) pcd_fms(v[q], S, qp, i, j);
+      }
+    }
+    if (l == (k & 31) && i >= k && i < b) {
+      while (*vstep != k) { }
+      __threadfence_block();
+      if (!S.fail) {
+        const uint32_t lkk = S.lkk;
+        const int qc = k >> 5;
+        pld::LD xs = v[0];
+#pragma unroll
+        for (int q = 1; q < PC_Q; q++)
+          if (q == qc) xs = v[q];
+        uint32_t xp;
+        if (i == k) {
+          xp = lkk;
+        } else {
+          LaneVal x;
+          lv_load(x, pld::ld_pattern(xs));
+          pg::Acc dv;
+          const bool dok = pg::acc_decode(lkk, dv) && dv.E <= 37 && dv.E >= -37;
+          bool done = false;
+          if (dok && x.dec) {
+            done = pg::acc_div(x.a, dv.M, dv.E, dv.sg, __drcp_rn((double)dv.M) * 4294967296.0, K);
+            if (done && !(x.a.E <= 75 && x.a.E >= -75) && x.a.E > pg::E_ZERO_LIMIT) {
+              x.pat = pg::acc_encode(x.a);
+              x.dec = false;
+            }
+          }
+          if (!done) lv_load(x, div(lv_pattern(x), lkk));
+          xp = lv_pattern(x);
+          uint32_t sp = 0u;
+          const double xd = pgd::stage_decode_d(xp, 0u, sp);
+          const uint8_t xf = sp == 0u ? 1 : 0;
+#pragma unroll
+          for (int r = 0; r < NC; r++) {
+            *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
+            *cl.map_shared_rank(&S.cold[qk][i], r) = xd;
+            *cl.map_shared_rank(&S.colf[qk][i], r) = xf;
+          }
+        }
+        pld::ld_load(xs, xp);
+#pragma unroll
+        for (int q = 0; q < PC_Q; q++)
+          if (q == qc) v[q] = xs;
+      }
+    }
+    __syncwarp();
+    pc_arrive();
+  }
+  if (!failed) pc_wait();
+#pragma unroll
+  for (int q = 0; q < PC_Q; q++) {
+    const int j = l + 32 * q;
+    if (i < b && j <= i) A[(int64_t)i * lda + j] = pld::ld_pattern(v[q]);
+  }
+  cl.sync();
+}
+
 }  // namespace pl
 
 using namespace pl;
@@ -397,6 +528,7 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     static PbOncePerDevice attrs;
     pb_once_per_device(attrs, [] {
       cudaFuncSetAttribute(k_potf2_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
     pb_count_launch();
     cudaLaunchConfig_t cfg = {};
@@ -412,8 +544,12 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const int32_t bb = (int32_t)b;
-    const cudaError_t e = nc == 16 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base)
-                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base);
+    const bool dm = pb_dpath();
+    const cudaError_t e =
+        nc == 16 ? (dm ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16>, A, lda, (int)bb, info, row_base)
+                       : cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base))
+                 : (dm ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8>, A, lda, (int)bb, info, row_base)
+                       : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base));
     return e == cudaSuccess ? 0 : POSIT_ECUDA;
   }
   if (mode >= 1 && b <= 256) {
