@@ -185,7 +185,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gflop/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
             "scaling": "strong" if args.gpus > 1 or args.workload != "gemm" else "weak", "vs_baseline": None,
-            "dtype": "posit32 (int32 ALU)", "data": "synthetic",
+            "dtype": "posit32 (CPU oracle: integer arithmetic)", "data": "synthetic",
             "config": _config(args, args.gpus, args.gpus > 1), "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -374,7 +374,7 @@ def run_ours(args):
             line = {"metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
                     "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                     "scaling": "strong" if dist_on else "weak",
-                    "vs_baseline": None, "dtype": "posit32 (int32 ALU; every mul/add correctly rounded)",
+                    "vs_baseline": None, "dtype": _dtype(),
                     "data": "synthetic (seeded numpy PCG64, BASELINE recipe)", "config": _config(args, world, dist_on),
                     "clocks": clocks, "gpu_launches": launches,
                     "parity": parity_vs_oracle("C2", Cfull.cpu().numpy()),
@@ -435,7 +435,7 @@ def run_ours(args):
             line = {"metric": METRIC, "value": r["value"], "unit": "Gflop/s", "n_gpus": world,
                     "steps": r["steps"], "warmup": r["warmup"], "ms_per_step": r["ms_per_step"],
                     "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                    "dtype": "posit32 (int32 ALU; every mul/add correctly rounded)",
+                    "dtype": _dtype(),
                     "data": "synthetic (seeded numpy PCG64, BASELINE recipe)",
                     "config": _config(args, world, dist_on), "clocks": r["clocks"],
                     "gpu_launches": r["gpu_launches"], "parity": r["parity"]}
@@ -486,6 +486,11 @@ def kernel_sass_sha(kernel_mangled: str):
         return None
     body = [l.strip() for l in txt.split("\n") if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l)]
     return hashlib.sha256("\n".join(body).encode()).hexdigest() if body else None
+
+
+def _dtype() -> str:
+    mac = "integer-pipe MAC" if os.environ.get("POSIT_GEMM_PATH", "1") == "0" else "binary64-pipe MAC"
+    return f"posit32 (every mul/add one correctly rounded Posit(32,2) op; {mac})"
 
 
 def gemm_roofline(PB, dA, dB, dC, dC0, m, n, k, stream):

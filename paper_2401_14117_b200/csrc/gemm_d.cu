@@ -38,7 +38,7 @@ struct CfgD {
     double b[2][BK][BN];
     uint32_t ra[BM * BK];             // raw patterns of the next slab (cp.async target, by quad)
     uint32_t rb[BK * BN];
-    pgd::dtab_t tab[pgd::DT_SIZE];    // M(E) by biased exponent
+    pgd::dtab_tt<pgd::T64_GEMM> tab[pgd::DT_SIZE];    // M(E) by biased exponent
   };
 };
 
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
   if (P.stop != nullptr && *P.stop != 0) return;
 
   const uint32_t flip = P.neg ? 1u : 0u;
-  for (int i = tid; i < pgd::DT_SIZE; i += NTHR) S.tab[i] = pgd::dtab_fill(i);   // visible after the first barrier
+  for (int i = tid; i < pgd::DT_SIZE; i += NTHR) S.tab[i] = pgd::dtab_fill<pgd::T64_GEMM>(i);   // visible after the first barrier
   const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(S.tab);
 
   double acc[TM][TN];
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) acc[i][j] = pgd::dmac(acc[i][j], av[i], bv[j], tab0);
+            for (int j = 0; j < TN; j++) acc[i][j] = pgd::dmac<pgd::T64_GEMM>(acc[i][j], av[i], bv[j], tab0);
         }
       } else {
         for (int kk = 0; kk < kmax; kk++) {
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 #pragma unroll
           for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < TN; j++) acc[i][j] = pgd::dmac(acc[i][j], av[i], bv[j], tab0);
+            for (int j = 0; j < TN; j++) acc[i][j] = pgd::dmac<pgd::T64_GEMM>(acc[i][j], av[i], bv[j], tab0);
         }
       }
     } else if (!bad) {
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 // operands inside their fast range; outside it the generic ops (same bits).
 __global__ void k_vec_d(int op, const uint32_t* a, const uint32_t* b, const uint32_t* c, uint32_t* out,
                         int64_t count) {
-  __shared__ pgd::dtab_t tab[pgd::DT_SIZE];
-  for (int i = threadIdx.x; i < pgd::DT_SIZE; i += blockDim.x) tab[i] = pgd::dtab_fill(i);
+  __shared__ pgd::dtab_tt<pgd::T64_GEMM> tab[pgd::DT_SIZE];
+  for (int i = threadIdx.x; i < pgd::DT_SIZE; i += blockDim.x) tab[i] = pgd::dtab_fill<pgd::T64_GEMM>(i);
   __syncthreads();
   const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
@@ -239,17 +239,17 @@ __global__ void k_vec_d(int op, const uint32_t* a, const uint32_t* b, const uint
     uint32_t r;
     if (op == POSIT_OP_DMUL) {
       const double da = pgd::stage_decode_d(x, 0u, sp), db = pgd::stage_decode_d(y, 0u, sp);
-      r = sp ? p32::mul(x, y) : pgd::d_encode(pgd::dmul_pos(da, db, tab0));
+      r = sp ? p32::mul(x, y) : pgd::d_encode(pgd::dmul_pos<pgd::T64_GEMM>(da, db, tab0));
     } else if (op == POSIT_OP_DADD) {
       // sum of two values of |E| <= 75 (a product's range): the D-MAC's sum step
       const double da = pgd::stage_decode_d<75>(x, 0u, sp), db = pgd::stage_decode_d<75>(y, 0u, sp);
-      r = sp ? p32::add(x, y) : pgd::d_encode(pgd::dadd_pos(da, db, tab0));
+      r = sp ? p32::add(x, y) : pgd::d_encode(pgd::dadd_pos<pgd::T64_GEMM>(da, db, tab0));
     } else {
       // out = c (+) (a (x) b) with |Ea|, |Eb| <= 37 and |Ec| <= 91
       double dc;
       const double da = pgd::stage_decode_d(x, 0u, sp), db = pgd::stage_decode_d(y, 0u, sp);
       const bool cok = pgd::d_decode(c[i], dc) && !pgd::d_above(dc, E_ACC_SLAB);
-      r = (sp || !cok) ? p32::add(c[i], p32::mul(x, y)) : pgd::d_encode(pgd::dmac(dc, da, db, tab0));
+      r = (sp || !cok) ? p32::add(c[i], p32::mul(x, y)) : pgd::d_encode(pgd::dmac<pgd::T64_GEMM>(dc, da, db, tab0));
     }
     out[i] = r;
   }

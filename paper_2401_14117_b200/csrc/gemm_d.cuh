@@ -37,6 +37,7 @@
 // everything else takes the generic per-operation path (same bits).
 #pragma once
 #include <stdint.h>
+#include <type_traits>
 #include "posit32.cuh"
 
 namespace pgd {
@@ -77,29 +78,44 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-// the table's element type and its fill value for entry i
-#if PGD_TAB32
-using dtab_t = uint32_t;
-__device__ __forceinline__ uint32_t dtab_fill(int i) { return (uint32_t)__double2hiint(dtab_entry(i)); }
-#else
-using dtab_t = double;
-__device__ __forceinline__ double dtab_fill(int i) { return dtab_entry(i); }
+// The table's element type, T64 = 8-byte entries (M itself, one LDS.64 into
+// the register pair) or 4-byte entries (M's hi word; the lo word is then
+// assembled, costing an IMAD.MOV per lookup, 1.31 per MAC in k_gemm_d's loop).
+// r2g A/B on C2: 8-byte 2810 vs 4-byte 2753 / 2743 Gflop/s, so the GEMM uses
+// T64 (PGD_GEMM_TAB64); the panel kernels keep 4-byte entries (PGD_TAB32) to
+// keep their shared-memory footprint (three Cholesky TRSM CTAs per SM).
+#ifndef PGD_GEMM_TAB64
+#define PGD_GEMM_TAB64 1
 #endif
+constexpr bool T64_PANEL = PGD_TAB32 == 0;
+constexpr bool T64_GEMM = PGD_GEMM_TAB64 != 0;
+template <bool T64>
+using dtab_tt = std::conditional_t<T64, double, uint32_t>;
+using dtab_t = dtab_tt<T64_PANEL>;
+
+// the table's fill value for entry i
+template <bool T64 = T64_PANEL>
+__device__ __forceinline__ dtab_tt<T64> dtab_fill(int i) {
+  if constexpr (T64) return dtab_entry(i);
+  else return (uint32_t)__double2hiint(dtab_entry(i));
+}
 
 // table entry for a binary64 hi word h (tab0: shared-memory byte address of entry 0)
+template <bool T64 = T64_PANEL>
 __device__ __forceinline__ double mtab_h(uint32_t h, uint32_t tab0) {
-#if PGD_TAB32
-  // lo word = the entry's byte offset: any lo word with an even last bit keeps
-  // M / q even and M inside its binade, and the offset register is live anyway
-  const uint32_t off = ((h >> 20) & 0x7FFu) << 2;
-  return __hiloint2double((int)lds_u32(tab0 + off), (int)off);
-#else
-  return lds_f64(tab0 + (((h >> 20) & 0x7FFu) << 3));
-#endif
+  if constexpr (!T64) {
+    // lo word = the entry's byte offset: any lo word with an even last bit keeps
+    // M / q even and M inside its binade, and the offset register is live anyway
+    const uint32_t off = ((h >> 20) & 0x7FFu) << 2;
+    return __hiloint2double((int)lds_u32(tab0 + off), (int)off);
+  } else {
+    return lds_f64(tab0 + (((h >> 20) & 0x7FFu) << 3));
+  }
 }
 
 // table entry of the binade of x
-__device__ __forceinline__ double mtab(double x, uint32_t tab0) { return mtab_h((uint32_t)__double2hiint(x), tab0); }
+template <bool T64 = T64_PANEL>
+__device__ __forceinline__ double mtab(double x, uint32_t tab0) { return mtab_h<T64>((uint32_t)__double2hiint(x), tab0); }
 
 // M(E) computed in registers: biased exponent eb + 25 + t(E), E = eb - 1023
 // (zero, eb = 0, gets a tiny normal M, which leaves 0 at 0)
@@ -125,8 +141,9 @@ __device__ __forceinline__ uint32_t odd_lo(uint32_t dlo, uint32_t ulo) {
 }
 
 // c (+) (a (x) b): a, b, c exact posit values in binary64, inside the fast range
+template <bool T64 = T64_PANEL>
 __device__ __forceinline__ double dmac(double c, double a, double b, uint32_t tab0) {
-  const double Mp = PGD_PROD_REG ? m_reg(__dmul_rn(a, b)) : mtab(__dmul_rn(a, b), tab0);
+  const double Mp = PGD_PROD_REG ? m_reg(__dmul_rn(a, b)) : mtab<T64>(__dmul_rn(a, b), tab0);
   const double P = __dsub_rn(__fma_rn(a, b, Mp), Mp);     // a (x) b
   const double d = __dadd_rd(c, P), u = __dadd_ru(c, P);
   const uint32_t dlo = (uint32_t)__double2loint(d), dhi = (uint32_t)__double2hiint(d);
@@ -135,24 +152,26 @@ __device__ __forceinline__ double dmac(double c, double a, double b, uint32_t ta
   // and the hi word of the odd one is the smaller hi word (a carry only leaves an odd p)
   const uint32_t ylo = odd_lo(dlo, ulo);
   const uint32_t yhi = umin(dhi, uhi);
-  const double Mc = mtab_h(dhi, tab0);
+  const double Mc = mtab_h<T64>(dhi, tab0);
   return __dsub_rn(__dadd_rn(__hiloint2double((int)yhi, (int)ylo), Mc), Mc);   // c (+) P
 }
 
 // c (+) P for an already rounded product P (the sum half of dmac)
+template <bool T64 = T64_PANEL>
 __device__ __forceinline__ double dadd_pos(double c, double P, uint32_t tab0) {
   const double d = __dadd_rd(c, P), u = __dadd_ru(c, P);
   const uint32_t dlo = (uint32_t)__double2loint(d), dhi = (uint32_t)__double2hiint(d);
   const uint32_t ulo = (uint32_t)__double2loint(u), uhi = (uint32_t)__double2hiint(u);
   const uint32_t ylo = odd_lo(dlo, ulo);
   const uint32_t yhi = umin(dhi, uhi);
-  const double Mc = mtab_h(dhi, tab0);
+  const double Mc = mtab_h<T64>(dhi, tab0);
   return __dsub_rn(__dadd_rn(__hiloint2double((int)yhi, (int)ylo), Mc), Mc);
 }
 
 // a (x) b (the product half of dmac)
+template <bool T64 = T64_PANEL>
 __device__ __forceinline__ double dmul_pos(double a, double b, uint32_t tab0) {
-  const double Mp = mtab(__dmul_rn(a, b), tab0);
+  const double Mp = mtab<T64>(__dmul_rn(a, b), tab0);
   return __dsub_rn(__fma_rn(a, b, Mp), Mp);
 }
 

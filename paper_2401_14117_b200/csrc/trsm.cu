@@ -651,6 +651,273 @@ __global__ void __launch_bounds__(FR_ROWS * W, MINB) k_trsm_rltn_fused(const uin
   }
 }
 
+// ---- right TRSM on the D-MAC, element-right-looking (Cholesky L21 = A21 L11^-T), n <= 256
+// Per row r of B the oracle's order (DESIGN Q6) is, for
+// i = 0 .. n-1:  x_i = b_i (/) L_ii,  then  b_j <- b_j (-) x_i (x) L_ji  for
+// every j > i  -- each element receives its updates one at a time in
+// ascending i, each (x), (-) and (/) one correctly rounded posit operation.
+// This kernel runs exactly that loop.  A row is held by a half-warp, lane c
+// owning columns c + 16 u (u = 0..15) as exact binary64 values in registers
+// (the u loop is unrolled, so the row never touches shared memory); the lane
+// owning column i divides (D-MAC division below), the quotient is broadcast
+// by a shuffle, and every lane advances its later columns with the binary64
+// MAC of gemm_d.cuh (L staged negated as binary64 in 32-column blocks, one
+// copy per CTA of 32 rows).  Range contract as the GEMM's: operands (L, x)
+// nonzero with |E| <= 37, every accumulator |E| <= 91 at each 16-step check.
+// A warp whose rows leave it stops at that step, keeps its state, and after
+// the loop finishes the row with the generic pattern operations from the same
+// state (same bits).
+constexpr int RD_ROWS = 32;                           // rows per CTA (16 warps, two rows each)
+constexpr int RD_KB = 32;                             // L columns staged per block
+constexpr int RD_LD = FR_NMAX + 1;
+
+struct RdSmem {
+  double l[RD_KB][RD_LD];                             // -L[j][c0 + k] (binary64, exact) at [k][j]
+  double dg[RD_KB];                                   // L[c0 + k][c0 + k]
+  double rc[RD_KB];                                   // RN(1 / L[c0 + k][c0 + k])
+  int bad[RD_KB];                                     // column c0 + k has a zero / NaR / |E| > 37 L value
+  pgd::dtab_tt<pgd::T64_GEMM> tab[pgd::DT_SIZE];
+};
+
+// q = b (/) d for exact posit values b (|E| <= 91) and d (fast operand) with
+// r = RN(1 / d): q1 = RN(b / d) refined once (faithful), e1 = b - q1 d exact
+// (fma; q1 within one ulp), so the exact quotient is q1 + e1 / d; y = the odd
+// one of q1 and its neighbour on that side (round to odd at 53 bits), then
+// RN(y + M) - M rounds it onto the posit lattice exactly as the exact quotient
+// (gemm_d.cuh, the sum's argument).  false: the quotient is not a fast operand.
+__device__ __forceinline__ bool rd_div(double b, double d, double r, double& x) {
+  const double q0 = __dmul_rn(b, r);
+  const double e0 = __fma_rn(-q0, d, b);
+  const double q1 = __fma_rn(e0, r, q0);
+  const double e1 = __fma_rn(-q1, d, b);
+  long long pq = __double_as_longlong(q1);
+  if (e1 != 0.0 && (pq & 1) == 0) {
+    // |exact| > |q1| iff e1 / d has q1's sign
+    const bool up = (__double_as_longlong(e1) ^ __double_as_longlong(d) ^ pq) >= 0;
+    pq += up ? 1 : -1;
+  }
+  const double y = __longlong_as_double(pq);
+  if (!pld::op_fast(y)) return false;
+  const double M = pgd::m_reg(y);
+  x = __dsub_rn(__dadd_rn(y, M), M);
+  return pld::op_fast(x);
+}
+
+__global__ void __launch_bounds__(RD_ROWS * 16, 2) k_trsm_rltn_d(const uint32_t* L, int64_t ldl, uint32_t* B,
+                                                                  int64_t ldb, int64_t m, int64_t n,
+                                                                  const int32_t* stop) {
+  constexpr int NT = RD_ROWS * 16;
+  extern __shared__ __align__(16) unsigned char rd_raw[];
+  RdSmem& S = *reinterpret_cast<RdSmem*>(rd_raw);
+  if (stop != nullptr && *stop != 0) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = lane & 15, hbase = lane & 16;          // column lane within the row; the row's first lane
+  const int64_t r = (int64_t)blockIdx.x * RD_ROWS + (tid >> 4);
+  const bool act = r < m;
+  const int nn = (int)n;
+  for (int i = tid; i < pgd::DT_SIZE; i += NT) S.tab[i] = pgd::dtab_fill<pgd::T64_GEMM>(i);
+  const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(S.tab);
+
+  // the row: b[u] = B[r][c + 16 u] as its exact binary64 value
+  double b[16];
+  bool okrow = true;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const int j = c + 16 * u;
+    const uint32_t x = (act && j < nn) ? B[r * ldb + j] : 0x40000000u;   // 1.0 in unused slots
+    okrow &= pgd::d_decode(x, b[u]) && !pgd::d_above(b[u], pg::E_ACC_SLAB);
+  }
+  bool slow = __any_sync(0xFFFFFFFFu, act && !okrow);
+  int i_slow = 0;                                       // first step the generic path redoes
+
+#pragma unroll
+  for (int t = 0; t < 16; t++) {
+    if (16 * t >= nn) continue;                         // CTA-uniform
+    if (t % 2 == 0) {                                   // stage L's columns [c0, c0 + 32)
+      const int c0 = 16 * t;
+      __syncthreads();
+      if (tid < RD_KB) S.bad[tid] = 0;
+      __syncthreads();
+      const int rows_l = nn - c0;
+      for (int e = tid; e < RD_KB * rows_l; e += NT) {
+        const int j = c0 + e / RD_KB, k = e % RD_KB;
+        if (c0 + k >= nn) continue;
+        const uint32_t x = L[(int64_t)j * ldl + c0 + k];
+        if (j > c0 + k) {
+          uint32_t sp = 0u;
+          S.l[k][j] = pgd::stage_decode_d(x, 1u, sp);
+          if (sp) atomicOr(&S.bad[k], 1);
+        } else if (j == c0 + k) {
+          uint32_t sp = 0u;
+          const double d = pgd::stage_decode_d(x, 0u, sp);
+          S.dg[k] = d;
+          S.rc[k] = sp ? 0.0 : __drcp_rn(d);
+          if (sp) atomicOr(&S.bad[k], 1);
+        }
+      }
+      __syncthreads();
+    }
+    if (!slow && t > 0) {                               // accumulator range check every 16 steps
+      bool hi = false;
+#pragma unroll
+      for (int u = t; u < 16; u++) hi |= pgd::d_above(b[u], pg::E_ACC_SLAB);
+      if (__any_sync(0xFFFFFFFFu, act && hi)) { slow = true; i_slow = 16 * t; }
+    }
+    if (!slow) {
+      const int iend = (nn - 16 * t) < 16 ? (nn - 16 * t) : 16;
+      for (int ii = 0; ii < iend; ii++) {
+        const int i = 16 * t + ii, k = i & (RD_KB - 1);
+        double xo = 0.0;
+        bool ok = S.bad[k] == 0;
+        if (c == ii && ok) ok = rd_div(b[t], S.dg[k], S.rc[k], xo);
+        if (__any_sync(0xFFFFFFFFu, act && !ok)) { slow = true; i_slow = i; break; }
+        const double x = __shfl_sync(0xFFFFFFFFu, xo, hbase + ii);
+        if (c == ii) b[t] = x;
+        if (c > ii && c + 16 * t < nn) b[t] = pgd::dmac<pgd::T64_GEMM>(b[t], x, S.l[k][c + 16 * t], tab0);
+#pragma unroll
+        for (int u = t + 1; u < 16; u++)
+          if (c + 16 * u < nn) b[u] = pgd::dmac<pgd::T64_GEMM>(b[u], x, S.l[k][c + 16 * u], tab0);
+      }
+    }
+  }
+  if (!slow) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+      if (act && c + 16 * u < nn) B[r * ldb + c + 16 * u] = pgd::d_encode(b[u]);
+    return;
+  }
+  // generic path from step i_slow on (state: columns < i_slow final, the rest
+  // updated by x_0 .. x_{i_slow - 1})
+#pragma unroll
+  for (int u = 0; u < 16; u++)
+    if (act && c + 16 * u < nn) B[r * ldb + c + 16 * u] = pgd::d_encode(b[u]);
+  __syncwarp();
+  for (int i = i_slow; i < nn; i++) {
+    const int o = i & 15;
+    uint32_t xo = 0u;
+    if (c == o && act) {
+      xo = p32::div(B[r * ldb + i], L[(int64_t)i * ldl + i]);
+      B[r * ldb + i] = xo;
+    }
+    const uint32_t x = __shfl_sync(0xFFFFFFFFu, xo, hbase + o);
+    if (act)
+      for (int j = c + 16 * ((i + 1 - c + 15) / 16); j < nn; j += 16)
+        if (j > i) B[r * ldb + j] = p32::sub(B[r * ldb + j], p32::mul(x, L[(int64_t)j * ldl + i]));
+  }
+}
+
+// ---- left TRSM on the D-MAC, element-right-looking (LU U12 = L11^-1 A12, unit diagonal), m <= 256
+// Per column of B the oracle's order (DESIGN Q6): for k = 0 .. m-1,
+// x_k = b_k is final, then b_i <- b_i (-) L_ik (x) x_k for every i > k
+// (ascending k per element, each operation one rounded posit op).  Same
+// machinery as k_trsm_rltn_d with rows and columns exchanged: a column of B
+// is held by a half-warp, lane c owning rows c + 16 u as binary64 registers;
+// 32 columns per CTA, staged in and out through shared memory (B is
+// row-major, so the column tile is read and written with coalesced rows);
+// -L[i][c0 + k] staged as binary64 at [k][i] in 32-column blocks.  No
+// division (unit diagonal).  A warp leaving the range contract stops at that
+// step and finishes with the generic pattern operations on the shared tile.
+constexpr int LD_COLS = 32;                           // columns of B per CTA (16 warps, two columns each)
+
+struct LdSmem {
+  union {
+    double l[RD_KB][RD_LD];                           // -L[i][c0 + k] at [k][i]
+    uint32_t t[FR_NMAX][LD_COLS + 1];                 // the CTA's columns of B (patterns), row-major
+  } u;
+  int bad[RD_KB];
+  pgd::dtab_tt<pgd::T64_GEMM> tab[pgd::DT_SIZE];
+};
+
+__global__ void __launch_bounds__(LD_COLS * 16, 2) k_trsm_llnu_d(const uint32_t* L, int64_t ldl, uint32_t* B,
+                                                                  int64_t ldb, int64_t m, int64_t n) {
+  constexpr int NT = LD_COLS * 16;
+  extern __shared__ __align__(16) unsigned char ld_raw[];
+  LdSmem& S = *reinterpret_cast<LdSmem*>(ld_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = lane & 15, hbase = lane & 16;          // row lane within the column; the column's first lane
+  const int cl = tid >> 4;                             // the CTA's column of this half-warp
+  const int64_t col0 = (int64_t)blockIdx.x * LD_COLS;
+  const int ncols = (n - col0) < LD_COLS ? (int)(n - col0) : LD_COLS;
+  const bool act = cl < ncols;
+  const int mm = (int)m;
+  for (int i = tid; i < pgd::DT_SIZE; i += NT) S.tab[i] = pgd::dtab_fill<pgd::T64_GEMM>(i);
+  const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(S.tab);
+  for (int e = tid; e < mm * LD_COLS; e += NT) {
+    const int i = e / LD_COLS, q = e % LD_COLS;
+    S.u.t[i][q] = q < ncols ? B[(int64_t)i * ldb + col0 + q] : 0x40000000u;
+  }
+  __syncthreads();
+  double b[16];
+  bool okcol = true;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const int i = c + 16 * u;
+    const uint32_t x = i < mm ? S.u.t[i][cl] : 0x40000000u;
+    okcol &= pgd::d_decode(x, b[u]) && !pgd::d_above(b[u], pg::E_ACC_SLAB);
+  }
+  bool slow = __any_sync(0xFFFFFFFFu, act && !okcol);
+  int k_slow = 0;
+
+#pragma unroll
+  for (int t = 0; t < 16; t++) {
+    if (16 * t >= mm) continue;                         // CTA-uniform
+    if (t % 2 == 0) {                                   // stage L's columns [c0, c0 + 32), rows below them
+      const int c0 = 16 * t;
+      __syncthreads();
+      if (tid < RD_KB) S.bad[tid] = 0;
+      __syncthreads();
+      const int rows_l = mm - c0;
+      for (int e = tid; e < RD_KB * rows_l; e += NT) {
+        const int i = c0 + e / RD_KB, k = e % RD_KB;
+        if (c0 + k >= mm || i <= c0 + k) continue;
+        uint32_t sp = 0u;
+        S.u.l[k][i] = pgd::stage_decode_d(L[(int64_t)i * ldl + c0 + k], 1u, sp);
+        if (sp) atomicOr(&S.bad[k], 1);
+      }
+      __syncthreads();
+    }
+    if (!slow && t > 0) {
+      bool hi = false;
+#pragma unroll
+      for (int u = t; u < 16; u++) hi |= pgd::d_above(b[u], pg::E_ACC_SLAB);
+      if (__any_sync(0xFFFFFFFFu, act && hi)) { slow = true; k_slow = 16 * t; }
+    }
+    if (!slow) {
+      const int kend = (mm - 16 * t) < 16 ? (mm - 16 * t) : 16;
+      for (int ii = 0; ii < kend; ii++) {
+        const int k = 16 * t + ii, kl = k & (RD_KB - 1);
+        const bool ok = S.bad[kl] == 0 && (c != ii || pld::op_fast(b[t]));
+        if (__any_sync(0xFFFFFFFFu, act && !ok)) { slow = true; k_slow = k; break; }
+        const double x = __shfl_sync(0xFFFFFFFFu, b[t], hbase + ii);
+        if (c > ii && c + 16 * t < mm) b[t] = pgd::dmac<pgd::T64_GEMM>(b[t], x, S.u.l[kl][c + 16 * t], tab0);
+#pragma unroll
+        for (int u = t + 1; u < 16; u++)
+          if (c + 16 * u < mm) b[u] = pgd::dmac<pgd::T64_GEMM>(b[u], x, S.u.l[kl][c + 16 * u], tab0);
+      }
+    }
+  }
+  __syncthreads();                                      // L staging done: the union holds B's tile again
+#pragma unroll
+  for (int u = 0; u < 16; u++)
+    if (act && c + 16 * u < mm) S.u.t[c + 16 * u][cl] = pgd::d_encode(b[u]);
+  if (slow) {
+    // generic path from step k_slow on (rows < k_slow final, the rest updated by x_0 .. x_{k_slow - 1});
+    // lane c reads and writes only its own rows, row k reaches the others by a shuffle
+    for (int k = k_slow; k < mm; k++) {
+      const uint32_t xo = (act && c == (k & 15)) ? S.u.t[k][cl] : 0u;
+      const uint32_t x = __shfl_sync(0xFFFFFFFFu, xo, hbase + (k & 15));
+      if (act)
+        for (int i = c + 16 * ((k + 1 - c + 15) / 16); i < mm; i += 16)
+          if (i > k) S.u.t[i][cl] = p32::sub(S.u.t[i][cl], p32::mul(L[(int64_t)i * ldl + k], x));
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * LD_COLS; e += NT) {
+    const int i = e / LD_COLS, q = e % LD_COLS;
+    if (q < ncols) B[(int64_t)i * ldb + col0 + q] = S.u.t[i][q];
+  }
+}
+
 }  // namespace pl
 
 using namespace pl;
@@ -675,6 +942,19 @@ int pb_trsm_llnu(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
     return e ? atoi(e) : 1;
   }();
   const bool g8 = pb_dpath() && g8_env != 0;
+  static const int d_env = [] {                   // POSIT_LLNU_D=0: the blocked kernels (in-block solves + GEMMs)
+    const char* e = getenv("POSIT_LLNU_D");
+    return e ? atoi(e) : 1;
+  }();
+  if (pb_dpath() && d_env != 0 && m <= FR_NMAX) {
+    static PbOncePerDevice attrs;
+    pb_once_per_device(attrs, [] {
+      cudaFuncSetAttribute(k_trsm_llnu_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LdSmem));
+    });
+    pb_count_launch();
+    k_trsm_llnu_d<<<(unsigned)((n + LD_COLS - 1) / LD_COLS), LD_COLS * 16, sizeof(LdSmem), st>>>(L, ldl, B, ldb, m, n);
+    return last_launch();
+  }
   for (int64_t i0 = 0; i0 < m; i0 += TB) {
     const int64_t ib = (m - i0) < TB ? (m - i0) : TB;
     if (ib > 1) {
@@ -728,12 +1008,20 @@ int pb_trsm_rltn(int64_t m, int64_t n, const uint32_t* L, int64_t ldl, uint32_t*
                            (int)sizeof(FrSmem<8, 32>));
       cudaFuncSetAttribute(k_trsm_rltn_fused<16, 16, FR_NMAX, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(FrSmem<16, 16, FR_NMAX, true>));
+      cudaFuncSetAttribute(k_trsm_rltn_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RdSmem));
     });
+    static const int rd_env = [] {                 // POSIT_RLTN_D=0: the blocked fused kernel on the D-MAC path
+      const char* e = getenv("POSIT_RLTN_D");
+      return e ? atoi(e) : 1;
+    }();
     pb_count_launch();
 #define PB_RLTN(W_, R_, ...)                                                                                         \
   k_trsm_rltn_fused<W_, R_, ##__VA_ARGS__><<<(unsigned)((m + R_ - 1) / R_), R_ * W_,                              \
                                               sizeof(FrSmem<W_, R_, ##__VA_ARGS__>), st>>>(L, ldl, B, ldb, m, n, stop, 1)
-    if (pb_dpath() && var == 1616)
+    if (pb_dpath() && var == 1616 && rd_env != 0)
+      k_trsm_rltn_d<<<(unsigned)((m + RD_ROWS - 1) / RD_ROWS), RD_ROWS * 16, sizeof(RdSmem), st>>>(L, ldl, B, ldb, m,
+                                                                                                 n, stop);
+    else if (pb_dpath() && var == 1616)
       k_trsm_rltn_fused<16, 16, FR_NMAX, 3, true><<<(unsigned)((m + 15) / 16), 256, sizeof(FrSmem<16, 16, FR_NMAX, true>),
                                                     st>>>(L, ldl, B, ldb, m, n, stop, 1);
     else if (var == 1632) PB_RLTN(16, 32);

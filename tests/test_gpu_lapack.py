@@ -54,6 +54,48 @@ def test_trsm_rltn_matches_oracle(cuda_ok):
         assert mismatch(to_host(dB), O.trsm_rltn(L, B)) == 0
 
 
+@pytest.mark.parametrize("m,n", [(1, 1), (33, 17), (75, 200), (97, 256), (64, 255)])
+def test_trsm_rltn_d_fast_slow_transitions(cuda_ok, m, n):
+    # the element-right-looking D-MAC kernel (k_trsm_rltn_d, n <= 256): rows
+    # scaled by 2^-s_r and a tiny diagonal entry at column n // 2 make the
+    # quotient leave the fast range at that step for some warps only (the
+    # generic path then finishes those rows from the same state); an exact
+    # zero below the diagonal at column 3n // 4 sends every warp to the
+    # generic path there; ragged m and n leave partial CTAs and column groups
+    import paper_2401_14117_b200 as PB
+    L64 = np.tril(SI.lu_matrix(n, 21), -1) + np.diag(1.0 + np.arange(n) % 3)
+    if n > 4:
+        L64[n // 2, n // 2] = 2.0 ** -45
+        L64[n - 1, (3 * n) // 4] = 0.0
+    s = np.random.default_rng(22).integers(0, 20, m)
+    B64 = SI.normal_matrix((m, n), 1.0, 23) * np.ldexp(1.0, -s)[:, None]
+    L, B = _pats(L64), _pats(B64)
+    dB = to_dev(B)
+    PB.posit_trsm("R", "L", "T", "N", to_dev(L), dB)
+    assert mismatch(to_host(dB), O.trsm_rltn(L, B)) == 0
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (17, 33), (200, 75), (256, 97), (255, 64), (256, 1000)])
+def test_trsm_llnu_d_fast_slow_transitions(cuda_ok, m, n):
+    # the element-right-looking D-MAC kernel (k_trsm_llnu_d, m <= 256):
+    # columns scaled by 2^s_c with a large entry at row m // 2 (x_k leaves the
+    # fast range there for some warps only), an exact zero in L below the
+    # diagonal of column 3m // 4 (every warp takes the generic path there),
+    # ragged m and n (partial column groups and CTAs)
+    import paper_2401_14117_b200 as PB
+    L64 = np.tril(SI.lu_matrix(m, 31), -1) + np.eye(m)
+    if m > 4:
+        L64[m - 1, (3 * m) // 4] = 0.0
+    s = np.random.default_rng(32).integers(0, 20, n)
+    B64 = SI.normal_matrix((m, n), 1.0, 33) * np.ldexp(1.0, s)[None, :]
+    if m > 4:
+        B64[m // 2, :] = np.ldexp(1.0, 25 + s)          # |E| > 37 for s > 12
+    L, B = _pats(L64), _pats(B64)
+    dB = to_dev(B)
+    PB.posit_trsm("L", "L", "N", "U", to_dev(L), dB)
+    assert mismatch(to_host(dB), O.trsm_llnu(L, B)) == 0
+
+
 def test_getrf_config1_bit_exact(cuda_ok):
     # configs[0]: n = 256, nb = 32, U[-1,1) seed 0
     A = _pats(SI.config1())

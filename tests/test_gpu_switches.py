@@ -101,12 +101,14 @@ LAPACK_SWITCHES = [
     {"POSIT_LEAF_COOP": "2"},
     {"POSIT_PANEL_LEAF": "64"},
     {"POSIT_LEAF_CTAS": "16"},
-    {"POSIT_LLNU_G8": "0", "POSIT_LLNU_COL": "0", "POSIT_LLNU_BLK": "32"},
-    {"POSIT_LLNU_G8": "0", "POSIT_LLNU_COL": "8"},
-    {"POSIT_LLNU_G8": "0"},
+    {"POSIT_LLNU_D": "0", "POSIT_LLNU_G8": "0", "POSIT_LLNU_COL": "0", "POSIT_LLNU_BLK": "32"},
+    {"POSIT_LLNU_D": "0", "POSIT_LLNU_G8": "0", "POSIT_LLNU_COL": "8"},
+    {"POSIT_LLNU_D": "0", "POSIT_LLNU_G8": "0"},
+    {"POSIT_LLNU_D": "0"},
     {"POSIT_RLTN": "8,16"},
     {"POSIT_RLTN": "16,32"},
     {"POSIT_RLTN": "16,16,128"},
+    {"POSIT_RLTN_D": "0"},
     {"POSIT_POTF2": "0"},
     {"POSIT_POTF2": "1"},
     {"POSIT_POTF2_NC": "16"},
