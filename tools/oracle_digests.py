@@ -81,7 +81,8 @@ def inputs(cfg: str):
     return {"A": O.from_f64_array(SI.config5(C5_NAMES[cfg]))}
 
 
-def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budget_s: float, chunk: int = 64):
+def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budget_s: float, chunk: int = 64,
+                     partial_path: str | None = None):
     """The textbook LU in chunks of `chunk` steps (or_getrf_steps: the same loop),
     checkpointed to ckpt_dir (A, ipiv, info, next step) when the time budget
     would run out; resumes from a checkpoint of the same input.  -> (LU, ipiv,
@@ -107,6 +108,16 @@ def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budge
             np.save(base + "_ipiv.npy", ipiv)
             json.dump({"k": k, "info": int(info[0]), "elapsed": time.time() - t0}, open(base + ".json", "w"))
             print(f"{cfg}: checkpoint at step {k} of {kmax} after {time.time() - t0:.0f} s", flush=True)
+            if partial_path:
+                # Right-looking LU: after steps 0..k-1, output rows 0..k-1 (U's row and the
+                # L entries left of the diagonal) and ipiv[0..k-1] are final -- later steps
+                # swap and update rows >= k only.  Their digests are already the full run's.
+                json.dump({"config": cfg, "partial_rows": k, "of_rows": int(A.shape[0]), "input_sha256": in_sha,
+                           "oracle_sha256": oracle_sha(), "ipiv_head_sha256": sha256(ipiv[:k]),
+                           "info_so_far": int(info[0]), "oracle_seconds": round(time.time() - t0, 1),
+                           "oracle_threads": O.num_threads(), "host": platform.node(),
+                           "digest_rule": "row i < partial_rows: sha256(row-major uint32 LE words of row i)[:16 hex]",
+                           "row_digests": row_digests(A[:k])}, open(partial_path, "w"), indent=0)
             return None
         tc = time.time()
         O.getrf_steps(A, ipiv, info, k, min(kmax, k + chunk))
@@ -158,7 +169,8 @@ def main() -> None:
         t0 = time.time()
         if args.ckpt_dir and cfg not in ("C2", "C3"):
             left = args.time_budget - (time.time() - T_START) if args.time_budget > 0 else 0.0
-            r = run_lu_resumable(cfg, X["A"], in_sha, args.ckpt_dir, left)
+            r = run_lu_resumable(cfg, X["A"], in_sha, args.ckpt_dir, left,
+                                  partial_path=os.path.join(args.out_dir, f"{cfg}_partial.json"))
             if r is None:
                 sys.exit(2)
             M, ipiv, info, dt_total = r
