@@ -257,9 +257,9 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 // element instead of 36), the updates on the D-MAC.  The division by l_kk and
 // the sqrt stay the integer-path operations (one per element / column).
 struct PcSmemD {
-  uint32_t colp[2][PC_B];                      // column k: patterns l_jk (rows j > k)
-  double cold[2][PC_B];                        // ... as binary64
-  uint8_t colf[2][PC_B];                       // ... fast-operand flags
+  uint32_t colp[3][PC_B];                      // column k: patterns l_jk (rows j > k); slot k % 3 (k & 1 if !DEFER)
+  double cold[3][PC_B];                        // ... as binary64
+  uint8_t colf[3][PC_B];                       // ... fast-operand flags
   int fail;
   int lkk_step;
   uint32_t lkk;
@@ -270,7 +270,17 @@ __device__ __forceinline__ void pcd_fms(pld::LD& x, const PcSmemD& S, int q, int
   pld::ld_fms(x, S.cold[q][i], S.colf[q][i] != 0, S.colp[q][i], S.cold[q][j], S.colf[q][j] != 0, S.colp[q][j]);
 }
 
-template <int NC>
+//
+// DEFER = 1 (POSIT_POTF2_DEFER; 0 is the default): column k's own slot is updated,
+// divided and published first; the column k - 1 update of the slots right of it
+// runs after the arrive, under the cluster barrier's latency (DEFER = 2: half of
+// them before, under the diagonal / sqrt latency, half after).  Element order is unchanged
+// (every element still takes column k - 1 before column k).  The column buffer
+// has three slots: a CTA still reads column k - 1 (slot (k - 1) % 3) after its
+// arrive of step k, and the next write of that slot is column k + 2's, which
+// follows the wait of step k + 2, i.e. every CTA's arrive of step k + 1, i.e.
+// the end of every CTA's deferred update of step k.
+template <int NC, int DEFER>
 __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
     k_potf2_cluster_d(uint32_t* A, int64_t lda, int b, int32_t* info, int64_t row_base) {
   namespace cg = cooperative_groups;
@@ -300,17 +310,19 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
   volatile int* vstep = &S.lkk_step;
   bool failed = false;
   for (int k = 0; k < b; k++) {
-    const int qk = k & 1, qp = qk ^ 1;
+    const int qk = DEFER ? k % 3 : (k & 1), qp = DEFER ? (k + 2) % 3 : (qk ^ 1);
+    const int qc = k >> 5;
     if (k > 0) {
       pc_wait();
-      if (S.fail) { failed = true; break; }
+      const int fs = *(volatile int*)&S.fail;                   // failing step + 1; a warp late to this wait
+      if (fs != 0 && fs <= k) { failed = true; break; }         // may already see step k's own failure: ignore it here
     }
     if (tid < b && tid >= k) {
       if (k > 0) pcd_fms(dd, S, qp, tid, tid);
       if (tid == k) {
         const uint32_t dk = pld::ld_pattern(dd);
         if ((int32_t)dk <= 0) {
-          S.fail = 1;
+          S.fail = k + 1;
           if (c == 0) *info = (int32_t)(row_base + k + 1);
         } else {
           S.lkk = p32::sqrt(dk);
@@ -323,7 +335,9 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 #pragma unroll
       for (int q = 0; q < PC_Q; q++) {
         const int j = l + 32 * q;
-        if (j >= k && j <= i) pcd_fms(v[q], S, qp, i, j);
+        // DEFER 0: every slot; 1: column k's slot; 2: column k's slot and the nearer half of the rest
+        const bool now = DEFER == 0 || q == qc || (DEFER == 2 && q <= qc + ((PC_Q - qc) >> 1));
+        if (now && j >= k && j <= i) pcd_fms(v[q], S, qp, i, j);
       }
     }
     if (l == (k & 31) && i >= k && i < b) {
@@ -331,7 +345,6 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
       __threadfence_block();
       if (!S.fail) {
         const uint32_t lkk = S.lkk;
-        const int qc = k >> 5;
         pld::LD xs = v[0];
 #pragma unroll
         for (int q = 1; q < PC_Q; q++)
@@ -372,6 +385,14 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
     }
     __syncwarp();
     pc_arrive();
+    if (DEFER && k > 0 && i < b) {                              // column k - 1 on the slots right of column k's
+#pragma unroll
+      for (int q = 1; q < PC_Q; q++) {
+        const int j = l + 32 * q;
+        const bool later = DEFER == 1 ? q > qc : q > qc + ((PC_Q - qc) >> 1);
+        if (later && j <= i) pcd_fms(v[q], S, qp, i, j);
+      }
+    }
   }
   if (!failed) pc_wait();
 #pragma unroll
@@ -520,15 +541,18 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     return e ? atoi(e) : 2;
   }();
   if (mode == 2 && b > TB && b <= PC_B) {
-    // POSIT_POTF2_NC: CTAs per cluster, 8 (portable; 32 row warps per CTA) or 16 (16 row warps)
+    // POSIT_POTF2_NC: CTAs per cluster, 16 (default since r2m: C3 86.9 -> 83.2 ms; non-portable
+    // size, 16 row warps per CTA) or 8 (portable; 32 row warps per CTA)
     static const int nc = [] {
       const char* e = getenv("POSIT_POTF2_NC");
-      return (e && atoi(e) == 16) ? 16 : 8;
+      return (e && atoi(e) == 8) ? 8 : 16;
     }();
     static PbOncePerDevice attrs;
     pb_once_per_device(attrs, [] {
       cudaFuncSetAttribute(k_potf2_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_potf2_cluster_d<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
     pb_count_launch();
     cudaLaunchConfig_t cfg = {};
@@ -545,11 +569,21 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     cfg.numAttrs = 1;
     const int32_t bb = (int32_t)b;
     const bool dm = pb_dpath();
+    // POSIT_POTF2_DEFER=0: the column k - 1 update of every slot before column k's division
+    static const int defer = [] {                 // r2n: 1 is slower than 0 (0.895 vs 0.745 ms per 256^2 block)
+      const char* e = getenv("POSIT_POTF2_DEFER");
+      const int v = e ? atoi(e) : 0;
+      return v == 1 || v == 2 ? v : 0;
+    }();
     const cudaError_t e =
-        nc == 16 ? (dm ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16>, A, lda, (int)bb, info, row_base)
-                       : cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base))
-                 : (dm ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8>, A, lda, (int)bb, info, row_base)
-                       : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base));
+        !dm ? (nc == 16 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base)
+                        : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base))
+        : nc == 16 ? (defer == 2   ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 2>, A, lda, (int)bb, info, row_base)
+                      : defer == 1 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 1>, A, lda, (int)bb, info, row_base)
+                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 0>, A, lda, (int)bb, info, row_base))
+                   : (defer == 2   ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 2>, A, lda, (int)bb, info, row_base)
+                      : defer == 1 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 1>, A, lda, (int)bb, info, row_base)
+                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 0>, A, lda, (int)bb, info, row_base));
     return e == cudaSuccess ? 0 : POSIT_ECUDA;
   }
   if (mode >= 1 && b <= 256) {
