@@ -248,6 +248,15 @@ int posit_to_f64(const uint32_t* p, double* out, int64_t count, void* stream);
  * operation at a time (every product and every sum rounded). */
 #define POSIT_OP_DADD 5
 #define POSIT_OP_DMUL 6
+/* The panel kernels' division and square root on the binary64 pipe (S:206-214:
+ * the Cholesky column scale l_ik = a_ik (/) l_kk and l_kk = sqrt(a_kk)), for the
+ * same one-operation check: 8 = div (dividend |scale| <= 91, divisor
+ * |scale| <= 37: faithful quotient + exact residual -> round to odd -> lattice;
+ * else the generic div), 9 = sqrt (a > 0, |scale| <= 75: correctly rounded root
+ * + exact residual -> round to odd -> lattice; else the generic sqrt; b unused).
+ * Same bits as 3 / 4.  (7 is posit_vec_dmac's internal code.) */
+#define POSIT_OP_DDIV 8
+#define POSIT_OP_DSQRT 9
 int posit_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream);
 
 /* out[i] = c[i] (+) (a[i] (x) b[i]): one step of the trailing update's chain

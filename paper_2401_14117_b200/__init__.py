@@ -25,7 +25,7 @@ __all__ = [
 POSIT_ONE = 0x40000000
 POSIT_MONE = 0xC0000000
 POSIT_NAR = 0x80000000
-OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "dadd": 5, "dmul": 6}
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "dadd": 5, "dmul": 6, "ddiv": 8, "dsqrt": 9}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("POSIT_LIB_PATH") or os.path.join(_HERE, "libposit_b200.so")

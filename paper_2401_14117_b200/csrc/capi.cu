@@ -614,7 +614,7 @@ int posit_to_f64(const uint32_t* p, double* out, int64_t count, void* stream) {
 }
 
 int posit_vec_op(int op, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream) {
-  if (op < POSIT_OP_ADD || op > POSIT_OP_DMUL) return -1;
+  if (op < POSIT_OP_ADD || op > POSIT_OP_DSQRT || op == 7) return -1;
   if (count < 0) return -5;
   if (count > 0 && (a == nullptr || b == nullptr || out == nullptr)) return -2;
   if (op >= POSIT_OP_DADD) return launch_check(pb_vec_d(op, a, b, nullptr, out, count, S(stream)));

@@ -263,6 +263,8 @@ struct PcSmemD {
   int fail;
   int lkk_step;
   uint32_t lkk;
+  int lkfast;                                  // l_kk is a fast operand: lkd, lkr valid (DDIV)
+  double lkd, lkr;                             // l_kk as binary64, RN(1 / l_kk)
   uint4 tx[pg::TSIZE];                         // the division's rounding table (integer path)
 };
 
@@ -273,14 +275,22 @@ __device__ __forceinline__ void pcd_fms(pld::LD& x, const PcSmemD& S, int q, int
 //
 // DEFER = 1 (POSIT_POTF2_DEFER; 0 is the default): column k's own slot is updated,
 // divided and published first; the column k - 1 update of the slots right of it
-// runs after the arrive, under the cluster barrier's latency (DEFER = 2: half of
-// them before, under the diagonal / sqrt latency, half after).  Element order is unchanged
+// runs after the arrive, under the cluster barrier's latency.  Measured slower
+// (r2n: 0.895 vs 0.745 ms per 256^2 block): the update was already hidden under
+// the diagonal thread's sqrt, and the barrier is short.
+//
+// DDIV (POSIT_POTF2_DDIV=1): the square root and the divisions on the
+// binary64 pipe (pld::sqrt_r, pld::div_r) while d_kk, l_kk and the dividend are
+// in the fast range, else the integer-path operations (same bits).  The r2m
+// profile of the integer-path kernel: one lane per row warp runs the ~400
+// instruction division, 8 warps per scheduler -- issue slots 53 % busy, ALU pipe
+// 47 %, FP64 pipe 4 %: the divisions, not the updates, were the column's cost.  Element order is unchanged
 // (every element still takes column k - 1 before column k).  The column buffer
 // has three slots: a CTA still reads column k - 1 (slot (k - 1) % 3) after its
 // arrive of step k, and the next write of that slot is column k + 2's, which
 // follows the wait of step k + 2, i.e. every CTA's arrive of step k + 1, i.e.
 // the end of every CTA's deferred update of step k.
-template <int NC, int DEFER>
+template <int NC, int DEFER, bool DDIV>
 __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
     k_potf2_cluster_d(uint32_t* A, int64_t lda, int b, int32_t* info, int64_t row_base) {
   namespace cg = cooperative_groups;
@@ -324,8 +334,21 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
         if ((int32_t)dk <= 0) {
           S.fail = k + 1;
           if (c == 0) *info = (int32_t)(row_base + k + 1);
+        } else if (DDIV && dd.dec) {
+          const double lk = pld::sqrt_r(dd.v);
+          S.lkk = pgd::d_encode(lk);
+          S.lkd = lk;
+          S.lkr = __drcp_rn(lk);
+          S.lkfast = pld::op_fast(lk) ? 1 : 0;
         } else {
           S.lkk = p32::sqrt(dk);
+          if (DDIV) {
+            double lk;
+            const bool ok = pgd::d_decode(S.lkk, lk) && lk != 0.0 && pld::op_fast(lk);
+            S.lkd = lk;
+            S.lkr = ok ? __drcp_rn(lk) : 0.0;
+            S.lkfast = ok ? 1 : 0;
+          }
         }
         __threadfence_block();
         *vstep = k;
@@ -335,8 +358,7 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 #pragma unroll
       for (int q = 0; q < PC_Q; q++) {
         const int j = l + 32 * q;
-        // DEFER 0: every slot; 1: column k's slot; 2: column k's slot and the nearer half of the rest
-        const bool now = DEFER == 0 || q == qc || (DEFER == 2 && q <= qc + ((PC_Q - qc) >> 1));
+        const bool now = DEFER == 0 || q == qc;                 // DEFER: column k's slot only
         if (now && j >= k && j <= i) pcd_fms(v[q], S, qp, i, j);
       }
     }
@@ -350,8 +372,19 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
         for (int q = 1; q < PC_Q; q++)
           if (q == qc) xs = v[q];
         uint32_t xp;
+        double xq;
+        bool dq = false;                                        // the quotient came from div_r
         if (i == k) {
           xp = lkk;
+        } else if (DDIV && S.lkfast && xs.dec && pld::div_r(xs.v, S.lkd, S.lkr, xq)) {
+          xp = pgd::d_encode(xq);                               // a fast operand: |E| <= 37, nonzero
+          dq = true;
+#pragma unroll
+          for (int r = 0; r < NC; r++) {
+            *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
+            *cl.map_shared_rank(&S.cold[qk][i], r) = xq;
+            *cl.map_shared_rank(&S.colf[qk][i], r) = (uint8_t)1;
+          }
         } else {
           LaneVal x;
           lv_load(x, pld::ld_pattern(xs));
@@ -377,7 +410,8 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
             *cl.map_shared_rank(&S.colf[qk][i], r) = xf;
           }
         }
-        pld::ld_load(xs, xp);
+        if (dq) { xs.v = xq; xs.pat = xp; xs.dec = true; }
+        else pld::ld_load(xs, xp);
 #pragma unroll
         for (int q = 0; q < PC_Q; q++)
           if (q == qc) v[q] = xs;
@@ -389,8 +423,7 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 #pragma unroll
       for (int q = 1; q < PC_Q; q++) {
         const int j = l + 32 * q;
-        const bool later = DEFER == 1 ? q > qc : q > qc + ((PC_Q - qc) >> 1);
-        if (later && j <= i) pcd_fms(v[q], S, qp, i, j);
+        if (q > qc && j <= i) pcd_fms(v[q], S, qp, i, j);
       }
     }
   }
@@ -550,9 +583,10 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     static PbOncePerDevice attrs;
     pb_once_per_device(attrs, [] {
       cudaFuncSetAttribute(k_potf2_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_potf2_cluster_d<16, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_potf2_cluster_d<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_potf2_cluster_d<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 0, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 0, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_potf2_cluster_d<16, 1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
     pb_count_launch();
     cudaLaunchConfig_t cfg = {};
@@ -570,20 +604,27 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     const int32_t bb = (int32_t)b;
     const bool dm = pb_dpath();
     // POSIT_POTF2_DEFER=0: the column k - 1 update of every slot before column k's division
-    static const int defer = [] {                 // r2n: 1 is slower than 0 (0.895 vs 0.745 ms per 256^2 block)
+    static const int defer = [] {                 // r2n / r2o: 1 is slower than 0 (0.895 vs 0.745 ms per 256^2 block)
       const char* e = getenv("POSIT_POTF2_DEFER");
-      const int v = e ? atoi(e) : 0;
-      return v == 1 || v == 2 ? v : 0;
+      return (e && atoi(e) == 1) ? 1 : 0;
     }();
-    const cudaError_t e =
-        !dm ? (nc == 16 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base)
-                        : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base))
-        : nc == 16 ? (defer == 2   ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 2>, A, lda, (int)bb, info, row_base)
-                      : defer == 1 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 1>, A, lda, (int)bb, info, row_base)
-                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<16, 0>, A, lda, (int)bb, info, row_base))
-                   : (defer == 2   ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 2>, A, lda, (int)bb, info, row_base)
-                      : defer == 1 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 1>, A, lda, (int)bb, info, row_base)
-                                   : cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<8, 0>, A, lda, (int)bb, info, row_base));
+    static const bool ddiv = [] {                 // POSIT_POTF2_DDIV=0: integer-path sqrt and divisions
+      const char* e = getenv("POSIT_POTF2_DDIV");
+      return e ? atoi(e) != 0 : false;   // opt-in until measured on the GPU
+    }();
+    cudaError_t e;
+#define PB_PC(NC_, DF_, DD_) e = cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<NC_, DF_, DD_>, A, lda, (int)bb, info, row_base)
+    if (!dm) e = nc == 16 ? cudaLaunchKernelEx(&cfg, k_potf2_cluster<16>, A, lda, (int)bb, info, row_base)
+                          : cudaLaunchKernelEx(&cfg, k_potf2_cluster<8>, A, lda, (int)bb, info, row_base);
+    else if (nc == 16 && defer == 0 && ddiv) PB_PC(16, 0, true);
+    else if (nc == 16 && defer == 0) PB_PC(16, 0, false);
+    else if (nc == 16 && ddiv) PB_PC(16, 1, true);
+    else if (nc == 16) PB_PC(16, 1, false);
+    else if (defer == 0 && ddiv) PB_PC(8, 0, true);
+    else if (defer == 0) PB_PC(8, 0, false);
+    else if (ddiv) PB_PC(8, 1, true);
+    else PB_PC(8, 1, false);
+#undef PB_PC
     return e == cudaSuccess ? 0 : POSIT_ECUDA;
   }
   if (mode >= 1 && b <= 256) {

@@ -17,6 +17,7 @@
 #include "gemm.cuh"
 #include "gemm_common.cuh"
 #include "gemm_d.cuh"
+#include "lanes_d.cuh"
 #include "internal.h"
 
 #ifndef PGD_KK_UNROLL
@@ -244,6 +245,17 @@ __global__ void k_vec_d(int op, const uint32_t* a, const uint32_t* b, const uint
       // sum of two values of |E| <= 75 (a product's range): the D-MAC's sum step
       const double da = pgd::stage_decode_d<75>(x, 0u, sp), db = pgd::stage_decode_d<75>(y, 0u, sp);
       r = sp ? p32::add(x, y) : pgd::d_encode(pgd::dadd_pos<pgd::T64_GEMM>(da, db, tab0));
+    } else if (op == POSIT_OP_DDIV) {
+      // a (/) b by the D-MAC division (dividend |E| <= 91, divisor a fast operand), else the generic div
+      double da, q;
+      const bool aok = pgd::d_decode(x, da) && !pgd::d_above(da, E_ACC_SLAB);
+      const double db = pgd::stage_decode_d(y, 0u, sp);
+      r = (aok && !sp && pld::div_r(da, db, __drcp_rn(db), q)) ? pgd::d_encode(q) : p32::div(x, y);
+    } else if (op == POSIT_OP_DSQRT) {
+      // sqrt(a) by the D-MAC square root (a > 0, |E| <= 75), else the generic sqrt
+      double da;
+      const bool aok = pgd::d_decode(x, da) && pld::in_lane_range(da) && da > 0.0;
+      r = aok ? pgd::d_encode(pld::sqrt_r(da)) : p32::sqrt(x);
     } else {
       // out = c (+) (a (x) b) with |Ea|, |Eb| <= 37 and |Ec| <= 91
       double dc;

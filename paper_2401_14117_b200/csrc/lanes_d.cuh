@@ -77,4 +77,44 @@ __device__ __forceinline__ void ld_fms(LD& c, double a, bool afast, uint32_t ap,
   }
 }
 
+// q = b (/) d for exact posit values b (|E| <= 91) and d (fast operand) with
+// r = RN(1 / d): q1 = RN(b / d) refined once (faithful), e1 = b - q1 d exact
+// (fma; q1 within one ulp), so the exact quotient is q1 + e1 / d; y = the odd
+// one of q1 and its neighbour on that side (round to odd at 53 bits), then
+// RN(y + M) - M rounds it onto the posit lattice exactly as the exact quotient
+// (gemm_d.cuh, the sum's argument).  false: the quotient is not a fast operand.
+__device__ __forceinline__ bool div_r(double b, double d, double r, double& x) {
+  const double q0 = __dmul_rn(b, r);
+  const double e0 = __fma_rn(-q0, d, b);
+  const double q1 = __fma_rn(e0, r, q0);
+  const double e1 = __fma_rn(-q1, d, b);
+  long long pq = __double_as_longlong(q1);
+  if (e1 != 0.0 && (pq & 1) == 0) {
+    // |exact| > |q1| iff e1 / d has q1's sign
+    const bool up = (__double_as_longlong(e1) ^ __double_as_longlong(d) ^ pq) >= 0;
+    pq += up ? 1 : -1;
+  }
+  const double y = __longlong_as_double(pq);
+  if (!op_fast(y)) return false;
+  const double M = pgd::m_reg(y);
+  x = __dsub_rn(__dadd_rn(y, M), M);
+  return op_fast(x);
+}
+
+// x = sqrt(d) for an exact posit value d > 0 with |E| <= 75: s = RN(sqrt d)
+// (correctly rounded), e = d - s s exact (fma: the residual of a correctly
+// rounded square root is representable), so the exact root is above s iff
+// e > 0; y = the odd one of s and its neighbour on that side (round to odd at
+// 53 bits), then RN(y + M) - M is the posit of the exact root (as div_r).
+// |E_x| <= 38: the caller checks op_fast(x) before using x as an operand.
+__device__ __forceinline__ double sqrt_r(double d) {
+  const double s = __dsqrt_rn(d);
+  const double e = __fma_rn(-s, s, d);
+  long long ps = __double_as_longlong(s);
+  if (e != 0.0 && (ps & 1) == 0) ps += e > 0.0 ? 1 : -1;
+  const double y = __longlong_as_double(ps);
+  const double M = pgd::m_reg(y);
+  return __dsub_rn(__dadd_rn(y, M), M);
+}
+
 }  // namespace pld

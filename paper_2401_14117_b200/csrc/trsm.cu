@@ -679,30 +679,7 @@ struct RdSmem {
   pgd::dtab_tt<pgd::T64_GEMM> tab[pgd::DT_SIZE];
 };
 
-// q = b (/) d for exact posit values b (|E| <= 91) and d (fast operand) with
-// r = RN(1 / d): q1 = RN(b / d) refined once (faithful), e1 = b - q1 d exact
-// (fma; q1 within one ulp), so the exact quotient is q1 + e1 / d; y = the odd
-// one of q1 and its neighbour on that side (round to odd at 53 bits), then
-// RN(y + M) - M rounds it onto the posit lattice exactly as the exact quotient
-// (gemm_d.cuh, the sum's argument).  false: the quotient is not a fast operand.
-__device__ __forceinline__ bool rd_div(double b, double d, double r, double& x) {
-  const double q0 = __dmul_rn(b, r);
-  const double e0 = __fma_rn(-q0, d, b);
-  const double q1 = __fma_rn(e0, r, q0);
-  const double e1 = __fma_rn(-q1, d, b);
-  long long pq = __double_as_longlong(q1);
-  if (e1 != 0.0 && (pq & 1) == 0) {
-    // |exact| > |q1| iff e1 / d has q1's sign
-    const bool up = (__double_as_longlong(e1) ^ __double_as_longlong(d) ^ pq) >= 0;
-    pq += up ? 1 : -1;
-  }
-  const double y = __longlong_as_double(pq);
-  if (!pld::op_fast(y)) return false;
-  const double M = pgd::m_reg(y);
-  x = __dsub_rn(__dadd_rn(y, M), M);
-  return pld::op_fast(x);
-}
-
+// the D-MAC division: pld::div_r (lanes_d.cuh)
 __global__ void __launch_bounds__(RD_ROWS * 16, 2) k_trsm_rltn_d(const uint32_t* L, int64_t ldl, uint32_t* B,
                                                                   int64_t ldb, int64_t m, int64_t n,
                                                                   const int32_t* stop) {
@@ -769,7 +746,7 @@ __global__ void __launch_bounds__(RD_ROWS * 16, 2) k_trsm_rltn_d(const uint32_t*
         const int i = 16 * t + ii, k = i & (RD_KB - 1);
         double xo = 0.0;
         bool ok = S.bad[k] == 0;
-        if (c == ii && ok) ok = rd_div(b[t], S.dg[k], S.rc[k], xo);
+        if (c == ii && ok) ok = pld::div_r(b[t], S.dg[k], S.rc[k], xo);
         if (__any_sync(0xFFFFFFFFu, act && !ok)) { slow = true; i_slow = i; break; }
         const double x = __shfl_sync(0xFFFFFFFFu, xo, hbase + ii);
         if (c == ii) b[t] = x;

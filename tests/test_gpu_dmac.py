@@ -133,6 +133,72 @@ def test_dmac_matches_oracle(cuda_ok):
     assert bad.size == 0, [(hex(C[i]), hex(A[i]), hex(B[i]), hex(got[i]), hex(ref[i])) for i in bad[:8]]
 
 
+def _div_pairs(seed, n=300000):
+    """dividends over the accumulator range, divisors over the operand range, plus
+    quotients built to sit on or next to a lattice midpoint / lattice point."""
+    rng = np.random.default_rng(seed)
+    parts_a, parts_b = [], []
+    parts_a.append(_scaled(rng, n, -75, 74)); parts_b.append(_scaled(rng, n, -37, 36))
+    # a = q (x) b exactly or a few patterns off: the quotient is a lattice point / near one
+    q = _scaled(rng, n, -30, 30)
+    b = _scaled(rng, n, -30, 30)
+    a = O.vec_op("mul", q, b)
+    d = rng.integers(-3, 4, n)
+    parts_a.append((a.astype(np.int64) + d).astype(np.uint32)); parts_b.append(b)
+    # quotients next to a midpoint of the quotient's lattice: a = (q + half a step) * b rounded
+    qv = O.to_f64_array(q)
+    qn = O.to_f64_array((q.astype(np.int64) + 1).astype(np.uint32))
+    mid = 0.5 * (qv + qn) * (1.0 + (rng.random(n) - 0.5) * np.exp2(-rng.integers(24, 50, n).astype(np.float64)))
+    parts_a.append(_pat(mid * O.to_f64_array(b))); parts_b.append(b)
+    # small-integer and power-of-two divisors (exact quotients, long carries)
+    parts_a.append(_scaled(rng, n // 2, -60, 60))
+    parts_b.append(_pat(np.where(rng.random(n // 2) < 0.5, -1.0, 1.0) * rng.integers(1, 64, n // 2).astype(np.float64)
+                        * np.exp2(rng.integers(-20, 21, n // 2).astype(np.float64))))
+    # Cholesky-like: |a| <~ |b|, b > 0 near 1 (l_ik = a_ik / l_kk)
+    parts_a.append(_pat(rng.standard_normal(n) * 0.05)); parts_b.append(_pat(1.0 + 0.2 * rng.random(n)))
+    # outside the fast range (generic fallback): zeros, NaR, extremes, raw patterns
+    E = SI.edge_patterns()
+    parts_a.append(np.repeat(E, E.size)); parts_b.append(np.tile(E, E.size))
+    parts_a.append(SI.random_patterns(50000, seed)); parts_b.append(SI.random_patterns(50000, seed + 1))
+    return np.concatenate(parts_a), np.concatenate(parts_b)
+
+
+def test_ddiv_matches_oracle(cuda_ok):
+    """The panel kernels' binary64-pipe division (pld::div_r), one operation at a time."""
+    import paper_2401_14117_b200 as PB
+    A, B = _div_pairs(15)
+    got = to_host(PB.posit_vec_op("ddiv", to_dev(A), to_dev(B)))
+    ref = O.vec_op("div", A, B)
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, [(hex(A[i]), hex(B[i]), hex(got[i]), hex(ref[i])) for i in bad[:8]]
+
+
+def test_dsqrt_matches_oracle(cuda_ok):
+    """The cluster potf2's binary64-pipe square root (pld::sqrt_r): random arguments over
+    |E| <= 75, exact squares and their pattern neighbours, arguments whose root sits
+    next to a midpoint of the root's lattice, and the generic fallback."""
+    import paper_2401_14117_b200 as PB
+    rng = np.random.default_rng(16)
+    n = 400000
+    parts = [_scaled(rng, n, -75, 74)]
+    r = _scaled(rng, n, -37, 36)
+    sq = O.vec_op("mul", r, r)                                   # rounded squares
+    parts.append((sq.astype(np.int64) + rng.integers(-3, 4, n)).astype(np.uint32))
+    r14 = _pat(rng.integers(1, 1 << 13, n).astype(np.float64) * np.exp2(rng.integers(-30, 20, n).astype(np.float64)))
+    parts.append(O.vec_op("mul", r14, r14))                      # exact squares (13-bit roots)
+    rv = np.abs(O.to_f64_array(r))
+    rn = np.abs(O.to_f64_array((r.astype(np.int64) + 1).astype(np.uint32)))
+    mid = 0.5 * (rv + rn) * (1.0 + (rng.random(n) - 0.5) * np.exp2(-rng.integers(24, 50, n).astype(np.float64)))
+    parts.append(_pat(mid * mid))
+    parts.append(_pat(1.0 + rng.random(n) * 3.0))                # Cholesky diagonals of configs[2]
+    parts.append(SI.edge_patterns()); parts.append(SI.random_patterns(100000, 17))
+    A = np.concatenate(parts)
+    got = to_host(PB.posit_vec_op("dsqrt", to_dev(A)))
+    ref = O.vec_op("sqrt", A, A)
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, [(hex(A[i]), hex(got[i]), hex(ref[i])) for i in bad[:8]]
+
+
 @pytest.mark.parametrize("path", ["0", "1"])
 def test_gemm_paths_identical_bits(cuda_ok, tmp_path, path):
     """The integer-MAC and binary64-MAC kernels give the oracle's bits on a GEMM

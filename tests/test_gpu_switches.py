@@ -113,9 +113,11 @@ LAPACK_SWITCHES = [
     {"POSIT_POTF2": "1"},
     {"POSIT_POTF2_NC": "8"},
     {"POSIT_POTF2_DEFER": "1"},
-    {"POSIT_POTF2_DEFER": "2"},
     {"POSIT_POTF2_DEFER": "1", "POSIT_POTF2_NC": "8"},
-    {"POSIT_POTF2_DEFER": "2", "POSIT_POTF2_NC": "8"},
+    {"POSIT_POTF2_DDIV": "0"},
+    {"POSIT_POTF2_DDIV": "1"},
+    {"POSIT_POTF2_DDIV": "1", "POSIT_POTF2_NC": "8"},
+    {"POSIT_POTF2_DDIV": "1", "POSIT_POTF2_DEFER": "1"},
     {"POSIT_GEMM_VARIANT": "12", "POSIT_GEMM_TINY": "2"},
     {"POSIT_GEMM_VARIANT": "13"},
     {"POSIT_GEMM_VARIANT": "14"},
