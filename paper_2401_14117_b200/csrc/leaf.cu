@@ -247,7 +247,8 @@ __device__ __forceinline__ void leaf_publish(const uint32_t* tile, int W, int64_
 template <int WMAX, bool DM = false>
 __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, int64_t m, int64_t w,
                                                      int64_t rows_per_cta, int32_t* ipiv, int32_t* info,
-                                                     int64_t row_base, LeafWs* ws, uint32_t* cand, uint32_t* jrow) {
+                                                     int64_t row_base, LeafWs* ws, uint32_t* cand, uint32_t* jrow,
+                                                     int ddiv) {
   extern __shared__ uint32_t tile[];                  // [rows_per_cta][w]
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long cbest;                // this CTA's best candidate key (next column)
@@ -333,8 +334,26 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
       pg::Acc dv;
       const bool dok = pg::acc_decode(v, dv) && v != 0x80000000u && dv.E <= 37 && dv.E >= -37;
       const double rcp = dok ? __drcp_rn((double)dv.M) * 4294967296.0 : 0.0;
+      // DM && ddiv: the column scale on the binary64 pipe (pld::div_r), else the integer-path division
+      double vd = 0.0, vr = 0.0;
+      bool vfast = false;
+      if constexpr (DM) {
+        if (ddiv) {
+          uint32_t sp = 0u;
+          vd = pgd::stage_decode_d(v, 0u, sp);
+          vfast = sp == 0u;
+          vr = vfast ? __drcp_rn(vd) : 0.0;
+        }
+      }
       for (int i = i0 + tid; i < nr; i += NT) {
         const uint32_t x = tile[i * W + (int)j];
+        if constexpr (DM) {
+          double xv, q;
+          if (vfast && pgd::d_decode(x, xv) && !pgd::d_above(xv, pg::E_ACC_SLAB) && pld::div_r(xv, vd, vr, q)) {
+            tile[i * W + (int)j] = pgd::d_encode(q);
+            continue;
+          }
+        }
         LaneVal t;
         lv_load(t, x);
         bool done = false;
@@ -450,7 +469,12 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     const bool wide_w = w > 64;
     uint32_t* cand = wide_w ? &ws->tcand[0][0][0] : &ws->cand[0][0][0];
     uint32_t* jrow = wide_w ? &ws->tjrow[0][0] : &ws->jrow[0][0];
-    void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws, &cand, &jrow};
+    static const int ddiv_env = [] {                // POSIT_LEAF_DDIV=1: the column scale by pld::div_r (D-MAC path)
+      const char* e = getenv("POSIT_LEAF_DDIV");
+      return e ? atoi(e) : 0;   // opt-in until measured on the GPU
+    }();
+    int ddiv = ddiv_env;
+    void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws, &cand, &jrow, &ddiv};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
     // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known; w <= 64)
     const void* kfn = nullptr;
