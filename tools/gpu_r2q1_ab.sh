@@ -1,0 +1,22 @@
+#!/bin/bash
+# GPU side of r2q1: element tests and A/B of the binary64-pipe division / sqrt in the
+# cluster potf2 (POSIT_POTF2_DDIV) and the LU leaf (POSIT_LEAF_DDIV).
+D=$1
+timeout 600 python -m pytest tests/test_gpu_dmac.py -m gpu -q -p no:cacheprovider > $D/pytest_dmac.log 2>&1; echo "dmac rc=$? $(tail -1 $D/pytest_dmac.log)" >> $D/sum.log
+for v in "" "POSIT_POTF2_DDIV=1" "POSIT_POTF2_DDIV=1 POSIT_POTF2_NC=8" "POSIT_POTF2_DDIV=1 POSIT_POTF2_DEFER=1"; do
+  echo "== $v" >> $D/potf2_once.log
+  env $v timeout 120 python tools/potf2_once.py >> $D/potf2_once.log 2>&1 || echo "FAILED rc=$? ($v)" >> $D/potf2_once.log
+done
+for v in "" "POSIT_POTF2_DDIV=1" "POSIT_POTF2_DDIV=1 POSIT_POTF2_DEFER=1"; do env $v TAG="$v" timeout 300 python tools/time_chol.py chol >> $D/factor.log 2>&1; done
+for v in "" "POSIT_LEAF_DDIV=1"; do env $v TAG="$v" timeout 300 python tools/time_chol.py lu >> $D/factor.log 2>&1; done
+for v in "" "POSIT_LEAF_DDIV=1"; do env $v TAG="$v" timeout 300 python tools/time_chol.py c4 >> $D/factor.log 2>&1; done
+for v in "POSIT_POTF2_DDIV=1" "POSIT_LEAF_DDIV=1" "POSIT_POTF2_DDIV=1 POSIT_LEAF_DDIV=1"; do
+  env $v timeout 900 python -m pytest tests/test_gpu_lapack.py -m gpu -q -p no:cacheprovider > $D/pytest_lapack.log 2>&1; echo "lapack [$v] rc=$? $(tail -1 $D/pytest_lapack.log)" >> $D/sum.log
+done
+timeout 900 python -m pytest tests/test_gpu_switches.py -m gpu -q -p no:cacheprovider -k "lapack_switches and (POTF2 or LEAF_DDIV)" > $D/pytest_sw.log 2>&1; echo "switches rc=$? $(tail -1 $D/pytest_sw.log)" >> $D/sum.log
+POSIT_POTF2_DDIV=1 timeout 600 python tests/config_parity.py --configs C3 --out $D/parity.jsonl > $D/parity.log 2>&1
+POSIT_LEAF_DDIV=1 timeout 900 python tests/config_parity.py --configs C1,C5m16,C5p0,C5p16 --out $D/parity.jsonl >> $D/parity.log 2>&1
+POSIT_POTF2_DDIV=1 timeout 600 python tools/chol_breakdown.py > $D/chol_breakdown_ddiv.log 2>&1
+POSIT_LEAF_DDIV=1 timeout 600 python tools/lu_breakdown.py > $D/lu_breakdown_ddiv.log 2>&1
+POSIT_POTF2_DDIV=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_potf2_cluster -s 3 -c 1 -o $D/prof_potf2_ddiv python tools/prof_factor.py chol 8192 > $D/ncu_potf2.log 2>&1
+cat $D/sum.log $D/potf2_once.log $D/factor.log

@@ -82,7 +82,7 @@ def inputs(cfg: str):
 
 
 def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budget_s: float, chunk: int = 64,
-                     partial_path: str | None = None):
+                     partial_path: str | None = None, ckpt_every: float = 0.0):
     """The textbook LU in chunks of `chunk` steps (or_getrf_steps: the same loop),
     checkpointed to ckpt_dir (A, ipiv, info, next step) when the time budget
     would run out; resumes from a checkpoint of the same input.  -> (LU, ipiv,
@@ -92,21 +92,30 @@ def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budge
     base = os.path.join(ckpt_dir, f"{cfg}_{in_sha[:16]}")
     if os.path.exists(base + ".json"):
         st = json.load(open(base + ".json"))
-        A = np.load(base + "_A.npy")
-        ipiv = np.load(base + "_ipiv.npy")
-        info = np.array([st["info"]], np.int32)
         k = st["k"]
+        A = np.load(base + f"_A_{k}.npy")
+        ipiv = np.load(base + f"_ipiv_{k}.npy")
+        info = np.array([st["info"]], np.int32)
         t0 -= st.get("elapsed", 0.0)                 # report the whole run's oracle time
         print(f"{cfg}: resuming at step {k} of {A.shape[0]} (checkpoint)", flush=True)
     else:
         A, ipiv, info, k = A0.copy(), np.zeros(min(A0.shape), np.int32), np.zeros(1, np.int32), 0
     kmax = min(A.shape)
     last = 0.0
+    t_ck = time.time()
     while k < kmax:
-        if budget_s > 0 and time.time() - t_call + 1.3 * last + 30 > budget_s:
-            np.save(base + "_A.npy", A)
-            np.save(base + "_ipiv.npy", ipiv)
-            json.dump({"k": k, "info": int(info[0]), "elapsed": time.time() - t0}, open(base + ".json", "w"))
+        stop = budget_s > 0 and time.time() - t_call + 1.3 * last + 30 > budget_s
+        if stop or (ckpt_every > 0 and time.time() - t_ck > ckpt_every and k > 0):
+            # the arrays of step k under their own names, then the index (.json) renamed into
+            # place: a kill at any point leaves the previous checkpoint whole
+            np.save(base + f"_A_{k}.npy", A)
+            np.save(base + f"_ipiv_{k}.npy", ipiv)
+            json.dump({"k": k, "info": int(info[0]), "elapsed": time.time() - t0}, open(base + ".tmp.json", "w"))
+            os.replace(base + ".tmp.json", base + ".json")
+            for f in os.listdir(ckpt_dir):
+                if f.startswith(os.path.basename(base) + "_") and f.endswith(".npy") and not f.endswith(f"_{k}.npy"):
+                    os.remove(os.path.join(ckpt_dir, f))
+            t_ck = time.time()
             print(f"{cfg}: checkpoint at step {k} of {kmax} after {time.time() - t0:.0f} s", flush=True)
             if partial_path:
                 # Right-looking LU: after steps 0..k-1, output rows 0..k-1 (U's row and the
@@ -117,15 +126,17 @@ def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budge
                            "info_so_far": int(info[0]), "oracle_seconds": round(time.time() - t0, 1),
                            "oracle_threads": O.num_threads(), "host": platform.node(),
                            "digest_rule": "row i < partial_rows: sha256(row-major uint32 LE words of row i)[:16 hex]",
-                           "row_digests": row_digests(A[:k])}, open(partial_path, "w"), indent=0)
-            return None
+                           "row_digests": row_digests(A[:k])}, open(partial_path + ".tmp", "w"), indent=0)
+                os.replace(partial_path + ".tmp", partial_path)
+            if stop:
+                return None
         tc = time.time()
         O.getrf_steps(A, ipiv, info, k, min(kmax, k + chunk))
         last = time.time() - tc
         k = min(kmax, k + chunk)
-    for f in (base + ".json", base + "_A.npy", base + "_ipiv.npy"):
-        if os.path.exists(f):
-            os.remove(f)
+    for f in os.listdir(ckpt_dir):
+        if f.startswith(os.path.basename(base)):
+            os.remove(os.path.join(ckpt_dir, f))
     return A, ipiv, int(info[0]), time.time() - t0
 
 
@@ -151,6 +162,7 @@ def main() -> None:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--ckpt-dir", default=None, help="LU configs: checkpoint / resume directory")
     ap.add_argument("--time-budget", type=float, default=0.0, help="seconds; checkpoint and stop before it runs out")
+    ap.add_argument("--ckpt-every", type=float, default=0.0, help="seconds between periodic checkpoints (0: only at the budget)")
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)
     os.makedirs(args.cache, exist_ok=True)
@@ -170,7 +182,8 @@ def main() -> None:
         if args.ckpt_dir and cfg not in ("C2", "C3"):
             left = args.time_budget - (time.time() - T_START) if args.time_budget > 0 else 0.0
             r = run_lu_resumable(cfg, X["A"], in_sha, args.ckpt_dir, left,
-                                  partial_path=os.path.join(args.out_dir, f"{cfg}_partial.json"))
+                                  partial_path=os.path.join(args.out_dir, f"{cfg}_partial.json"),
+                                  ckpt_every=args.ckpt_every)
             if r is None:
                 sys.exit(2)
             M, ipiv, info, dt_total = r
