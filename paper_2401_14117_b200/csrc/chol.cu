@@ -256,10 +256,22 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 // holding {binary64 value, fast flag, pattern} (8 + 1 + 4 bytes pushed per
 // element instead of 36), the updates on the D-MAC.  The division by l_kk and
 // the sqrt stay the integer-path operations (one per element / column).
+#ifndef PC_PACKED                               // 1: one 16-byte {binary64, pattern, flag} entry per column element
+#define PC_PACKED 0                             //    (one remote store per CTA instead of three, one LDS.128 per operand)
+#endif
+struct __align__(16) PcCol {
+  double d;
+  uint32_t p;
+  uint32_t f;
+};
 struct PcSmemD {
+#if PC_PACKED
+  PcCol col[3][PC_B];                          // column k: l_jk (rows j > k); slot k % 3 (k & 1 if !DEFER)
+#else
   uint32_t colp[3][PC_B];                      // column k: patterns l_jk (rows j > k); slot k % 3 (k & 1 if !DEFER)
   double cold[3][PC_B];                        // ... as binary64
   uint8_t colf[3][PC_B];                       // ... fast-operand flags
+#endif
   int fail;
   int lkk_step;
   uint32_t lkk;
@@ -269,7 +281,30 @@ struct PcSmemD {
 };
 
 __device__ __forceinline__ void pcd_fms(pld::LD& x, const PcSmemD& S, int q, int i, int j) {
+#if PC_PACKED
+  const uint4 a = *reinterpret_cast<const uint4*>(&S.col[q][i]), b = *reinterpret_cast<const uint4*>(&S.col[q][j]);
+  pld::ld_fms(x, __hiloint2double((int)a.y, (int)a.x), a.w != 0u, a.z, __hiloint2double((int)b.y, (int)b.x), b.w != 0u,
+              b.z);
+#else
   pld::ld_fms(x, S.cold[q][i], S.colf[q][i] != 0, S.colp[q][i], S.cold[q][j], S.colf[q][j] != 0, S.colp[q][j]);
+#endif
+}
+
+// push l_ik = {pattern xp, binary64 xd, fast flag xf} into slot q of every CTA's column buffer
+template <int NC, class CL>
+__device__ __forceinline__ void pcd_push(CL& cl, PcSmemD& S, int q, int i, uint32_t xp, double xd, uint32_t xf) {
+#if PC_PACKED
+  const uint4 e = make_uint4((uint32_t)__double2loint(xd), (uint32_t)__double2hiint(xd), xp, xf);
+#pragma unroll
+  for (int r = 0; r < NC; r++) *reinterpret_cast<uint4*>(cl.map_shared_rank(&S.col[q][i], r)) = e;
+#else
+#pragma unroll
+  for (int r = 0; r < NC; r++) {
+    *cl.map_shared_rank(&S.colp[q][i], r) = xp;
+    *cl.map_shared_rank(&S.cold[q][i], r) = xd;
+    *cl.map_shared_rank(&S.colf[q][i], r) = (uint8_t)xf;
+  }
+#endif
 }
 
 //
@@ -379,12 +414,7 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
         } else if (DDIV && S.lkfast && xs.dec && pld::div_r(xs.v, S.lkd, S.lkr, xq)) {
           xp = pgd::d_encode(xq);                               // a fast operand: |E| <= 37, nonzero
           dq = true;
-#pragma unroll
-          for (int r = 0; r < NC; r++) {
-            *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
-            *cl.map_shared_rank(&S.cold[qk][i], r) = xq;
-            *cl.map_shared_rank(&S.colf[qk][i], r) = (uint8_t)1;
-          }
+          pcd_push<NC>(cl, S, qk, i, xp, xq, 1u);
         } else {
           LaneVal x;
           lv_load(x, pld::ld_pattern(xs));
@@ -402,13 +432,7 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
           xp = lv_pattern(x);
           uint32_t sp = 0u;
           const double xd = pgd::stage_decode_d(xp, 0u, sp);
-          const uint8_t xf = sp == 0u ? 1 : 0;
-#pragma unroll
-          for (int r = 0; r < NC; r++) {
-            *cl.map_shared_rank(&S.colp[qk][i], r) = xp;
-            *cl.map_shared_rank(&S.cold[qk][i], r) = xd;
-            *cl.map_shared_rank(&S.colf[qk][i], r) = xf;
-          }
+          pcd_push<NC>(cl, S, qk, i, xp, xd, sp == 0u ? 1u : 0u);
         }
         if (dq) { xs.v = xq; xs.pat = xp; xs.dec = true; }
         else pld::ld_load(xs, xp);

@@ -19,4 +19,17 @@ POSIT_LEAF_DDIV=1 timeout 900 python tests/config_parity.py --configs C1,C5m16,C
 POSIT_POTF2_DDIV=1 timeout 600 python tools/chol_breakdown.py > $D/chol_breakdown_ddiv.log 2>&1
 POSIT_LEAF_DDIV=1 timeout 600 python tools/lu_breakdown.py > $D/lu_breakdown_ddiv.log 2>&1
 POSIT_POTF2_DDIV=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_potf2_cluster -s 3 -c 1 -o $D/prof_potf2_ddiv python tools/prof_factor.py chol 8192 > $D/ncu_potf2.log 2>&1
+# the packed column buffer (-DPC_PACKED=1) as a second library
+V=$PWD/paper_2401_14117_b200/ab/libposit_pcpack.so
+if [ -f $V ]; then
+  for v in "" "POSIT_POTF2_DDIV=1" "POSIT_POTF2_DDIV=1 POSIT_POTF2_NC=8"; do
+    echo "== pcpack $v" >> $D/potf2_once.log
+    env POSIT_LIB_PATH=$V $v timeout 120 python tools/potf2_once.py >> $D/potf2_once.log 2>&1 || echo "FAILED rc=$? (pcpack $v)" >> $D/potf2_once.log
+  done
+  for v in "" "POSIT_POTF2_DDIV=1"; do env POSIT_LIB_PATH=$V $v TAG="pcpack $v" timeout 300 python tools/time_chol.py chol >> $D/factor.log 2>&1; done
+  for v in "" "POSIT_POTF2_DDIV=1"; do
+    env POSIT_LIB_PATH=$V $v timeout 900 python -m pytest tests/test_gpu_lapack.py -m gpu -q -p no:cacheprovider -k "potrf or chol or potf2" > $D/pytest_pcpack.log 2>&1; echo "pcpack lapack [$v] rc=$? $(tail -1 $D/pytest_pcpack.log)" >> $D/sum.log
+    env POSIT_LIB_PATH=$V $v timeout 600 python tests/config_parity.py --configs C3 --out $D/parity_pcpack.jsonl >> $D/parity_pcpack.log 2>&1
+  done
+fi
 cat $D/sum.log $D/potf2_once.log $D/factor.log
