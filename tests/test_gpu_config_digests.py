@@ -22,7 +22,7 @@ import sys
 
 import pytest
 
-from tests.config_parity import ALL, DIGESTS, compare
+from tests.config_parity import ALL, DIGESTS, compare, compare_partial
 
 pytestmark = pytest.mark.gpu
 
@@ -36,6 +36,18 @@ def test_config_every_word_matches_oracle(cuda_ok, cfg):
     assert rep["input_sha_match"], rep
     assert rep["mismatched_rows"] == 0, rep
     assert rep["ok"], rep
+
+
+PARTIAL = [c for c in ALL if c not in PRESENT and os.path.exists(os.path.join(DIGESTS, f"{c}_partial.json"))]
+
+
+@pytest.mark.parametrize("cfg", PARTIAL)
+def test_config_final_rows_match_oracle(cuda_ok, cfg):
+    """An LU config whose oracle run was checkpointed after k steps (<cfg>_partial.json):
+    output rows < k (every column) and ipiv[:k] are final there and must match."""
+    rep = compare_partial(cfg)
+    assert rep["input_sha_match"], rep
+    assert rep["mismatched_rows"] == 0 and rep["ipiv_match"], rep
 
 
 SERIAL = [{"POSIT_LOOKAHEAD": "0"}, {"POSIT_PDL": "0"}, {"POSIT_LOOKAHEAD": "0", "POSIT_PDL": "0"}]
