@@ -5,6 +5,12 @@
 START=${1:-1}; END=${2:-3}
 for i in $(seq $START $END); do
   T=r2q$i
+  # between calls: up to ${GO_WAIT:-230} s for the operator to read the last call's results and
+  # prepare this call's queue script / defaults (touch /tmp/go_$i to start at once); the box is
+  # kept for 5 min after a call, and the oracle checkpoint lives in its /tmp
+  if [ $i -gt $START ]; then
+    w=0; while [ ! -f /tmp/go_$i ] && [ $w -lt ${GO_WAIT:-230} ]; do sleep 2; w=$((w+2)); done
+  fi
   GS=""; [ -f tools/gpu_queue/$i.sh ] && GS=tools/gpu_queue/$i.sh
   while true; do
     gpurun --timeout 3600 -- "TAGDIR=$T GPU_SCRIPT=$GS ORACLE_BUDGET=${OB:-3250} bash tools/gpu_r2q_chunk.sh" > /tmp/chunk_$T.log 2>&1
