@@ -32,4 +32,10 @@ if [ -f $V ]; then
     env POSIT_LIB_PATH=$V $v timeout 600 python tests/config_parity.py --configs C3 --out $D/parity_pcpack.jsonl >> $D/parity_pcpack.log 2>&1
   done
 fi
-cat $D/sum.log $D/potf2_once.log $D/factor.log
+# GEMM tile A/B on C2 (D1 64x128 / 1024 threads / 1 CTA per SM is the model's choice; r2m ncu: 7 % of the
+# stall samples at the slab barrier): D2 64x64, D3 32x128, D4 128x32 with 512 threads, 2 CTAs per SM
+for v in 21 22 23 24; do
+  POSIT_GEMM_VARIANT=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-factor-keys > $D/ab_tmp.log 2>&1
+  echo "variant=$v $(grep '^{' $D/ab_tmp.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["parity"]["mismatches"])')" >> $D/gemm_variant_ab.log
+done
+cat $D/sum.log $D/potf2_once.log $D/factor.log $D/gemm_variant_ab.log
