@@ -27,10 +27,16 @@
 namespace pg {
 
 constexpr int KK_UNROLL_D = PGD_KK_UNROLL;
+#ifndef PGD_BK                       // k-slab depth: one CTA barrier (and one special-operand check) per slab
+#define PGD_BK 16
+#endif
+// accumulator |E| limit at a slab start: one MAC raises |E| by at most 1 and the sum needs |E| <= 107
+constexpr int E_ACC_SLAB_D = 107 - PGD_BK;
+static_assert(E_ACC_SLAB_D <= E_ACC_SLAB && PGD_BK % 4 == 0, "slab depth");
 
 template <int BM_, int BN_, int TM_, int TN_, int MINB_, int EFF100 = 100>
 struct CfgD {
-  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = 16, MINB = MINB_;
+  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = PGD_BK, MINB = MINB_;
   static constexpr double EFF = EFF100 / 100.0;
   static constexpr int NTX = BN / TN, NTY = BM / TM, NTHR = NTX * NTY;
   static constexpr int AQN = BM * BK / 4, BQN = BN * BK / 4;
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 #pragma unroll
       for (int i = 0; i < TM; i++)
 #pragma unroll
-        for (int j = 0; j < TN; j++) bad = bad | pgd::d_above(acc[i][j], E_ACC_SLAB);
+        for (int j = 0; j < TN; j++) bad = bad | pgd::d_above(acc[i][j], E_ACC_SLAB_D);
       if (kmax == BK) {
 #pragma unroll KK_UNROLL_D
         for (int kk = 0; kk < BK; kk++) {

@@ -38,4 +38,17 @@ for v in 21 22 23 24; do
   POSIT_GEMM_VARIANT=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-factor-keys > $D/ab_tmp.log 2>&1
   echo "variant=$v $(grep '^{' $D/ab_tmp.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["parity"]["mismatches"])')" >> $D/gemm_variant_ab.log
 done
+# k-slab depth 32 (half the CTA barriers) as a second library
+V2=$PWD/paper_2401_14117_b200/ab/libposit_bk32.so
+if [ -f $V2 ]; then
+  for v in 21 22; do
+    POSIT_LIB_PATH=$V2 POSIT_GEMM_VARIANT=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-factor-keys > $D/ab_tmp.log 2>&1
+    echo "bk32 variant=$v $(grep '^{' $D/ab_tmp.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["parity"]["mismatches"])')" >> $D/gemm_variant_ab.log
+  done
+  POSIT_LIB_PATH=$V2 TAG=bk32 timeout 300 python tools/time_chol.py chol >> $D/factor.log 2>&1
+  POSIT_LIB_PATH=$V2 TAG=bk32 timeout 300 python tools/time_chol.py lu >> $D/factor.log 2>&1
+  POSIT_LIB_PATH=$V2 TAG=bk32 timeout 300 python tools/time_chol.py c4 >> $D/factor.log 2>&1
+  POSIT_LIB_PATH=$V2 timeout 900 python -m pytest tests/test_gpu_gemm.py -m gpu -q -p no:cacheprovider > $D/pytest_bk32.log 2>&1; echo "bk32 gemm tests rc=$? $(tail -1 $D/pytest_bk32.log)" >> $D/sum.log
+  POSIT_LIB_PATH=$V2 timeout 900 python tests/config_parity.py --configs C2,C3,C5p0 --out $D/parity_bk32.jsonl > $D/parity_bk32.log 2>&1
+fi
 cat $D/sum.log $D/potf2_once.log $D/factor.log $D/gemm_variant_ab.log
