@@ -698,11 +698,14 @@ __global__ void __launch_bounds__(RD_ROWS * 16, 2) k_trsm_rltn_d(const uint32_t*
   // the row: b[u] = B[r][c + 16 u] as its exact binary64 value
   double b[16];
   bool okrow = true;
+  uint32_t narm = 0u;                                   // NaR has no binary64 image: kept as a mask (a NaR
+                                                        // makes the row slow from step 0, so b[] is never advanced)
 #pragma unroll
   for (int u = 0; u < 16; u++) {
     const int j = c + 16 * u;
     const uint32_t x = (act && j < nn) ? B[r * ldb + j] : 0x40000000u;   // 1.0 in unused slots
     okrow &= pgd::d_decode(x, b[u]) && !pgd::d_above(b[u], pg::E_ACC_SLAB);
+    if (x == p32::NAR) narm |= 1u << u;
   }
   bool slow = __any_sync(0xFFFFFFFFu, act && !okrow);
   int i_slow = 0;                                       // first step the generic path redoes
@@ -767,7 +770,7 @@ __global__ void __launch_bounds__(RD_ROWS * 16, 2) k_trsm_rltn_d(const uint32_t*
   // updated by x_0 .. x_{i_slow - 1})
 #pragma unroll
   for (int u = 0; u < 16; u++)
-    if (act && c + 16 * u < nn) B[r * ldb + c + 16 * u] = pgd::d_encode(b[u]);
+    if (act && c + 16 * u < nn) B[r * ldb + c + 16 * u] = ((narm >> u) & 1u) ? p32::NAR : pgd::d_encode(b[u]);
   __syncwarp();
   for (int i = i_slow; i < nn; i++) {
     const int o = i & 15;
@@ -826,11 +829,14 @@ __global__ void __launch_bounds__(LD_COLS * 16, 2) k_trsm_llnu_d(const uint32_t*
   __syncthreads();
   double b[16];
   bool okcol = true;
+  uint32_t narm = 0u;                                   // NaR has no binary64 image: kept as a mask (a NaR
+                                                        // makes the column slow from step 0, so b[] is never advanced)
 #pragma unroll
   for (int u = 0; u < 16; u++) {
     const int i = c + 16 * u;
     const uint32_t x = i < mm ? S.u.t[i][cl] : 0x40000000u;
     okcol &= pgd::d_decode(x, b[u]) && !pgd::d_above(b[u], pg::E_ACC_SLAB);
+    if (x == p32::NAR) narm |= 1u << u;
   }
   bool slow = __any_sync(0xFFFFFFFFu, act && !okcol);
   int k_slow = 0;
@@ -876,7 +882,7 @@ __global__ void __launch_bounds__(LD_COLS * 16, 2) k_trsm_llnu_d(const uint32_t*
   __syncthreads();                                      // L staging done: the union holds B's tile again
 #pragma unroll
   for (int u = 0; u < 16; u++)
-    if (act && c + 16 * u < mm) S.u.t[c + 16 * u][cl] = pgd::d_encode(b[u]);
+    if (act && c + 16 * u < mm) S.u.t[c + 16 * u][cl] = ((narm >> u) & 1u) ? p32::NAR : pgd::d_encode(b[u]);
   if (slow) {
     // generic path from step k_slow on (rows < k_slow final, the rest updated by x_0 .. x_{k_slow - 1});
     // lane c reads and writes only its own rows, row k reaches the others by a shuffle
