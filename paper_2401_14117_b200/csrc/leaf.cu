@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
       double vd = 0.0, vr = 0.0;
       bool vfast = false;
       if constexpr (DM) {
-        if (ddiv) {
+        if (ddiv & 1) {
           uint32_t sp = 0u;
           vd = pgd::stage_decode_d(v, 0u, sp);
           vfast = sp == 0u;
@@ -365,7 +365,38 @@ __global__ void __launch_bounds__(1024) k_leaf_coop1(uint32_t* A, int64_t lda, i
     const int wq = W - (int)j - 1;
     if (wq > 0) {
       unsigned long long best = 0ull;
-      const uint32_t cnt = nr > i0 ? (uint32_t)(nr - i0) * (uint32_t)wq : 0u;
+      uint32_t cnt = nr > i0 ? (uint32_t)(nr - i0) * (uint32_t)wq : 0u;
+      if constexpr (DM) {
+        // Row mode (ddiv & 2; tall CTAs: at least half the threads own a row): a thread takes whole
+        // rows, so the multiplier l_ij is decoded once per row and there is no element -> (row, column)
+        // division; lanes walk the columns in a rotated order (lane + t mod wq), which spreads one
+        // column's rows (stride W words: one bank) over the banks.  Same single update per element.
+        if ((ddiv & 2) && (nr - i0) * 2 >= NT) {
+          const int start = (int)((uint32_t)(tid & 31) % (uint32_t)wq);
+          for (int i = i0 + tid; i < nr; i += NT) {
+            const uint32_t lp = tile[i * W + (int)j];
+            uint32_t sp = 0u;
+            const double l = pgd::stage_decode_d(lp, 0u, sp);
+            int qq = start;
+            for (int t = 0; t < wq; t++) {
+              const int q = (int)j + 1 + qq;
+              qq = qq + 1 == wq ? 0 : qq + 1;
+              const uint32_t cx = tile[i * W + q];
+              double cv;
+              const bool cd = pgd::d_decode(cx, cv) && pld::in_lane_range(cv);
+              const uint32_t nv = (sp == 0u && urowf[q] != 0 && cd)
+                                      ? pgd::d_encode(pgd::dmac(cv, l, urowd[q], dtab0))
+                                      : sub(cx, mul(lp, urowp[q]));
+              tile[i * W + q] = nv;
+              if (q == (int)j + 1) {
+                const unsigned long long k = piv_key(nv, rb + i);
+                best = k > best ? k : best;
+              }
+            }
+          }
+          cnt = 0u;
+        }
+      }
       for (uint32_t e = tid; e < cnt; e += NT) {
         const uint32_t ii = e / (uint32_t)wq;
         const int i = i0 + (int)ii;
@@ -473,7 +504,11 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
       const char* e = getenv("POSIT_LEAF_DDIV");
       return e ? atoi(e) : 0;   // opt-in until measured on the GPU
     }();
-    int ddiv = ddiv_env;
+    static const int rows_env = [] {                // POSIT_LEAF_ROWS=1: a thread per row in the update of tall CTAs
+      const char* e = getenv("POSIT_LEAF_ROWS");
+      return e ? atoi(e) : 0;   // opt-in until measured on the GPU
+    }();
+    int ddiv = (ddiv_env ? 1 : 0) | (rows_env ? 2 : 0);
     void* args[] = {&A, &ld, &mm, &ww, &rr, &ipiv, &info, &rbase, &ws, &cand, &jrow, &ddiv};
     const unsigned grid = (unsigned)((m + rpc - 1) / rpc);
     // coop 1: one grid sync per column (default); coop 2: two (publish after the pivot is known; w <= 64)

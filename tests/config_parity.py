@@ -32,7 +32,7 @@ DIGESTS = os.path.join(ROOT, "tests", "golden", "config_digests")
 C5_NAMES = {"C5m16": -16, "C5m4": -4, "C5p0": 0, "C5p4": 4, "C5p16": 16}
 ALL = ["C1", "C2", "C3"] + list(C5_NAMES) + ["C4"]
 SWITCHES = ("POSIT_GEMM_PATH", "POSIT_LOOKAHEAD", "POSIT_PDL", "POSIT_GEMM_VARIANT", "POSIT_RLTN", "POSIT_RLTN_D", "POSIT_POTF2", "POSIT_POTF2_NC", "POSIT_POTF2_DEFER", "POSIT_POTF2_DDIV",
-            "POSIT_PANEL_LEAF", "POSIT_LEAF_DDIV", "POSIT_LEAF_COOP", "POSIT_LLNU_COL", "POSIT_LLNU_G8", "POSIT_LLNU_D", "POSIT_TAIL_W")
+            "POSIT_PANEL_LEAF", "POSIT_LEAF_DDIV", "POSIT_LEAF_ROWS", "POSIT_LEAF_COOP", "POSIT_LLNU_COL", "POSIT_LLNU_G8", "POSIT_LLNU_D", "POSIT_TAIL_W")
 
 
 def _sha(*arrays) -> str:
