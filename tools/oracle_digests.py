@@ -82,7 +82,7 @@ def inputs(cfg: str):
 
 
 def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budget_s: float, chunk: int = 64,
-                     partial_path: str | None = None, ckpt_every: float = 0.0):
+                     partial_path: str | None = None, ckpt_every: float = 0.0, stop_after_chunks: int = 0):
     """The textbook LU in chunks of `chunk` steps (or_getrf_steps: the same loop),
     checkpointed to ckpt_dir (A, ipiv, info, next step) when the time budget
     would run out; resumes from a checkpoint of the same input.  -> (LU, ipiv,
@@ -103,8 +103,10 @@ def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budge
     kmax = min(A.shape)
     last = 0.0
     t_ck = time.time()
+    chunks_done = 0
     while k < kmax:
-        stop = budget_s > 0 and time.time() - t_call + 1.3 * last + 30 > budget_s
+        stop = (budget_s > 0 and time.time() - t_call + 1.3 * last + 30 > budget_s) or \
+               (stop_after_chunks > 0 and chunks_done >= stop_after_chunks)      # the latter: tests
         if stop or (ckpt_every > 0 and time.time() - t_ck > ckpt_every and k > 0):
             # the arrays of step k under their own names, then the index (.json) renamed into
             # place: a kill at any point leaves the previous checkpoint whole
@@ -134,6 +136,7 @@ def run_lu_resumable(cfg: str, A0: np.ndarray, in_sha: str, ckpt_dir: str, budge
         O.getrf_steps(A, ipiv, info, k, min(kmax, k + chunk))
         last = time.time() - tc
         k = min(kmax, k + chunk)
+        chunks_done += 1
     for f in os.listdir(ckpt_dir):
         if f.startswith(os.path.basename(base)):
             os.remove(os.path.join(ckpt_dir, f))
