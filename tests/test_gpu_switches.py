@@ -102,10 +102,11 @@ LAPACK_SWITCHES = [
     {"POSIT_PANEL_LEAF": "64"},
     {"POSIT_LEAF_CTAS": "16"},
     {"POSIT_LEAF_DDIV": "1"},
-    # one 1024-thread CTA per side-stream leaf: tall CTAs (>= 512 rows), where the row-mode update applies
-    {"POSIT_SIDE_LEAF_CTAS": "1"},
-    {"POSIT_LEAF_ROWS": "1", "POSIT_SIDE_LEAF_CTAS": "1"},
-    {"POSIT_LEAF_ROWS": "1", "POSIT_LEAF_DDIV": "1", "POSIT_SIDE_LEAF_CTAS": "1"},
+    # one 1024-thread CTA per side-stream leaf, never the wide leaf on the side stream: tall CTAs
+    # (>= 512 rows in the first lookahead panels), where the row-mode update applies
+    {"POSIT_WIDE_LEAF_COLS": "0", "POSIT_SIDE_LEAF_CTAS": "1"},
+    {"POSIT_LEAF_ROWS": "1", "POSIT_WIDE_LEAF_COLS": "0", "POSIT_SIDE_LEAF_CTAS": "1"},
+    {"POSIT_LEAF_ROWS": "1", "POSIT_LEAF_DDIV": "1", "POSIT_WIDE_LEAF_COLS": "0", "POSIT_SIDE_LEAF_CTAS": "1"},
     {"POSIT_LEAF_ROWS": "1", "POSIT_LEAF_DDIV": "1"},
     {"POSIT_LEAF_DDIV": "1", "POSIT_LEAF_CTAS": "16"},
     {"POSIT_LLNU_D": "0", "POSIT_LLNU_G8": "0", "POSIT_LLNU_COL": "0", "POSIT_LLNU_BLK": "32"},
