@@ -36,11 +36,13 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-o", LIB, *sources()]
+    tmp = LIB + ".building"                      # link elsewhere, then rename: the .so in place is always whole
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-o", tmp, *sources()]
     if verbose:
         cmd += ["-Xptxas", "-v"]
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
     return LIB
 
 
