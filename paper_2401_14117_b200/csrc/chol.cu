@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32 * (PC_B / NC), 1)
 // element instead of 36), the updates on the D-MAC.  The division by l_kk and
 // the sqrt stay the integer-path operations (one per element / column).
 #ifndef PC_PACKED                               // 1: one 16-byte {binary64, pattern, flag} entry per column element
-#define PC_PACKED 0                             //    (one remote store per CTA instead of three, one LDS.128 per operand)
+#define PC_PACKED 1                             //    (one remote store per CTA instead of three, one LDS.128 per operand)
 #endif
 struct __align__(16) PcCol {
   double d;
@@ -634,7 +634,7 @@ int pb_potf2(int64_t b, uint32_t* A, int64_t lda, int32_t* info, int64_t row_bas
     }();
     static const bool ddiv = [] {                 // POSIT_POTF2_DDIV=0: integer-path sqrt and divisions
       const char* e = getenv("POSIT_POTF2_DDIV");
-      return e ? atoi(e) != 0 : false;   // opt-in until measured on the GPU
+      return e ? atoi(e) != 0 : true;   // measured: see DESIGN.md section 8
     }();
     cudaError_t e;
 #define PB_PC(NC_, DF_, DD_) e = cudaLaunchKernelEx(&cfg, k_potf2_cluster_d<NC_, DF_, DD_>, A, lda, (int)bb, info, row_base)

@@ -28,7 +28,7 @@ namespace pg {
 
 constexpr int KK_UNROLL_D = PGD_KK_UNROLL;
 #ifndef PGD_BK                       // k-slab depth: one CTA barrier (and one special-operand check) per slab
-#define PGD_BK 16
+#define PGD_BK 32
 #endif
 // accumulator |E| limit at a slab start: one MAC raises |E| by at most 1 and the sum needs |E| <= 107
 constexpr int E_ACC_SLAB_D = 107 - PGD_BK;

@@ -502,7 +502,7 @@ static int getrf_leaf(int64_t m, int64_t w, uint32_t* A, int64_t lda, int32_t* i
     uint32_t* jrow = wide_w ? &ws->tjrow[0][0] : &ws->jrow[0][0];
     static const int ddiv_env = [] {                // POSIT_LEAF_DDIV=1: the column scale by pld::div_r (D-MAC path)
       const char* e = getenv("POSIT_LEAF_DDIV");
-      return e ? atoi(e) : 0;   // opt-in until measured on the GPU
+      return e ? atoi(e) : 1;   // measured: see DESIGN.md section 8
     }();
     static const int rows_env = [] {                // POSIT_LEAF_ROWS=1: a thread per row in the update of tall CTAs
       const char* e = getenv("POSIT_LEAF_ROWS");
