@@ -27,16 +27,24 @@
 namespace pg {
 
 constexpr int KK_UNROLL_D = PGD_KK_UNROLL;
-#ifndef PGD_BK                       // k-slab depth: one CTA barrier (and one special-operand check) per slab
-#define PGD_BK 32
+// k-slab depth (one CTA barrier and one special-operand check per slab).  r2q1 A/B: with one
+// 1024-thread CTA per SM (D1) a barrier idles the SM, and 32-deep slabs gain (C2 2802 -> 2903
+// Gflop/s, C4 1126.7 -> 1092.5 ms); with two 512-thread CTAs per SM (D2..D4, the SYRK's tiles) the
+// other CTA covers the barrier and 16 stays ahead (C3 83.5 vs 84.4 ms).
+#ifndef PGD_BK
+#define PGD_BK 32                    // tiles with one CTA per SM
 #endif
-// accumulator |E| limit at a slab start: one MAC raises |E| by at most 1 and the sum needs |E| <= 107
-constexpr int E_ACC_SLAB_D = 107 - PGD_BK;
-static_assert(E_ACC_SLAB_D <= E_ACC_SLAB && PGD_BK % 4 == 0, "slab depth");
+#ifndef PGD_BK2
+#define PGD_BK2 16                   // tiles with two CTAs per SM
+#endif
+static_assert(PGD_BK % 4 == 0 && PGD_BK2 % 4 == 0 && 107 - PGD_BK <= E_ACC_SLAB && 107 - PGD_BK2 <= E_ACC_SLAB,
+              "slab depth");
 
 template <int BM_, int BN_, int TM_, int TN_, int MINB_, int EFF100 = 100>
 struct CfgD {
-  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = PGD_BK, MINB = MINB_;
+  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, BK = MINB_ == 1 ? PGD_BK : PGD_BK2, MINB = MINB_;
+  // accumulator |E| limit at a slab start: one MAC raises |E| by at most 1 and the sum needs |E| <= 107
+  static constexpr int E_SLAB = 107 - BK;
   static constexpr double EFF = EFF100 / 100.0;
   static constexpr int NTX = BN / TN, NTY = BM / TM, NTHR = NTX * NTY;
   static constexpr int AQN = BM * BK / 4, BQN = BN * BK / 4;
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) k_gemm_d(Params P) {
 #pragma unroll
       for (int i = 0; i < TM; i++)
 #pragma unroll
-        for (int j = 0; j < TN; j++) bad = bad | pgd::d_above(acc[i][j], E_ACC_SLAB_D);
+        for (int j = 0; j < TN; j++) bad = bad | pgd::d_above(acc[i][j], C::E_SLAB);
       if (kmax == BK) {
 #pragma unroll KK_UNROLL_D
         for (int kk = 0; kk < BK; kk++) {

@@ -26,7 +26,7 @@ for a in sys.argv[1:]:
     elif k == "pc_packed":
         sub(os.path.join(C, "chol.cu"), r"#define PC_PACKED [01]", f"#define PC_PACKED {v}")
     elif k == "bk":
-        sub(os.path.join(C, "gemm_d.cu"), r"#define PGD_BK \d+", f"#define PGD_BK {v}")
+        sub(os.path.join(C, "gemm_d.cu"), r"#define PGD_BK \d+ ", f"#define PGD_BK {v} ")
     elif k == "potf2_defer":
         sub(os.path.join(C, "chol.cu"), r'(getenv\("POSIT_POTF2_DEFER"\);\s*return \(e && atoi\(e\) == 1\) \? 1 : )0;',
             r"\g<1>0;" if v == "0" else r"\g<1>0;")
