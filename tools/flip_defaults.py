@@ -23,6 +23,9 @@ for a in sys.argv[1:]:
     elif k == "leaf_ddiv":
         sub(os.path.join(C, "leaf.cu"), r'(getenv\("POSIT_LEAF_DDIV"\);\s*return e \? atoi\(e\) : )[01];[^\n]*',
             r"\g<1>" + v + ";   // measured: see DESIGN.md section 8")
+    elif k == "leaf_rows":
+        sub(os.path.join(C, "leaf.cu"), r'(getenv\("POSIT_LEAF_ROWS"\);\s*return e \? atoi\(e\) : )[01];[^\n]*',
+            r"\g<1>" + v + ";   // measured: see DESIGN.md section 8")
     elif k == "pc_packed":
         sub(os.path.join(C, "chol.cu"), r"#define PC_PACKED [01]", f"#define PC_PACKED {v}")
     elif k == "bk":
