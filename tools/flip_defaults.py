@@ -26,6 +26,12 @@ for a in sys.argv[1:]:
     elif k == "leaf_rows":
         sub(os.path.join(C, "leaf.cu"), r'(getenv\("POSIT_LEAF_ROWS"\);\s*return e \? atoi\(e\) : )[01];[^\n]*',
             r"\g<1>" + v + ";   // measured: see DESIGN.md section 8")
+    elif k == "wide_leaf_cols":
+        sub(os.path.join(C, "capi.cu"), r'(getenv\("POSIT_WIDE_LEAF_COLS"\);\s*return e \? \(int64_t\)atoll\(e\) : \(int64_t\))\d+;',
+            r"\g<1>" + v + ";")
+    elif k == "side_min":
+        sub(os.path.join(C, "leaf.cu"), r"const int64_t side_auto = \(m \+ 1023\) / 1024 < \d+ \? \d+ :",
+            f"const int64_t side_auto = (m + 1023) / 1024 < {v} ? {v} :")
     elif k == "pc_packed":
         sub(os.path.join(C, "chol.cu"), r"#define PC_PACKED [01]", f"#define PC_PACKED {v}")
     elif k == "bk":
